@@ -1,0 +1,155 @@
+/*
+ * igabem_b200.h -- C ABI of the B200-native H² boundary-element operator.
+ *
+ * Drop-in boundary for the reference's hot path (igabem v0.1.0,
+ * /root/reference/proj/core): Galerkin assembly and application of the
+ * H²-compressed single-layer (Laplace, Helmholtz) and EFIE (Maxwell) operator.
+ * Each entry point names the reference interface it replaces.  Plain
+ * pointers and sizes only; complex scalars are interleaved (re, im) doubles,
+ * i.e. the memory of std::complex<double> / Eigen::VectorXcd.  Every call
+ * returns a status code mapping the reference's exception types:
+ *   IGB_INVALID_ARGUMENT <- std::invalid_argument   (e.g. h2.cpp:102-110,257)
+ *   IGB_LOGIC_ERROR      <- std::logic_error        (e.g. h2.cpp:82,88)
+ *   IGB_RUNTIME_ERROR    <- std::runtime_error      (e.g. spaces.cpp:99-104)
+ *   IGB_DOMAIN_ERROR     <- std::domain_error       (splines.cpp:62)
+ *   IGB_CUDA_ERROR       device failure (no reference analogue)
+ * igb_last_error() returns the message of the last failure on this thread.
+ */
+#ifndef IGABEM_B200_H
+#define IGABEM_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  IGB_OK = 0,
+  IGB_INVALID_ARGUMENT = 1,
+  IGB_LOGIC_ERROR = 2,
+  IGB_RUNTIME_ERROR = 3,
+  IGB_DOMAIN_ERROR = 4,
+  IGB_CUDA_ERROR = 5
+};
+/* Pde::Kind (pde.hpp:10) */
+enum { IGB_LAPLACE = 0, IGB_HELMHOLTZ = 1, IGB_MAXWELL = 2 };
+/* PairClass (quadrature.hpp:17) */
+enum { IGB_FAR = 0, IGB_VERTEX = 1, IGB_EDGE = 2, IGB_COINCIDENT = 3 };
+
+typedef struct igb_geometry igb_geometry;
+typedef struct igb_discretization igb_discretization;
+typedef struct igb_h2 igb_h2;
+
+/* PatchSurface (splines.hpp:53-67): clamped knot vectors, homogeneous
+ * control points ctrl_w (3 doubles per point, point i + j*count_u) and
+ * positive weights. */
+typedef struct {
+  int degree_u, degree_v;
+  int n_knots_u, n_knots_v;
+  const double* knots_u;
+  const double* knots_v;
+  const double* ctrl_w;
+  const double* weight;
+} igb_patch_desc;
+
+/* Geometry(std::vector<PatchSurface>)  geometry.hpp:40 (topology inference,
+ * regularity and orientation checks, geometry.cpp:88-163) */
+int igb_geometry_create(int n_patches, const igb_patch_desc* patches, igb_geometry** out);
+/* make_sphere(radius, center)  shapes.hpp:21, shapes.cpp:87-205 */
+int igb_geometry_sphere(double radius, const double center[3], igb_geometry** out);
+/* make_square()  shapes.hpp:16, shapes.cpp:28-30 */
+int igb_geometry_square(igb_geometry** out);
+/* patch_count(), edge_idents().size(), vertex_idents().size()  geometry.hpp:42-45 */
+int igb_geometry_info(const igb_geometry* g, int* n_patches, int* n_edges, int* n_vertices);
+void igb_geometry_destroy(igb_geometry* g);
+
+/* Discretization(geometry, Pde{kind, kappa}, degree, rep, level)
+ * spaces.hpp:39-40, spaces.cpp:71-115; pde.hpp:19-25 */
+int igb_discretization_create(const igb_geometry* g, int kind, double kappa_re, double kappa_im,
+                              int degree, int rep, int level, igb_discretization** out);
+typedef struct {
+  int dof_count, element_count, local_count, level, degree, repetition, kind, patch_count;
+} igb_disc_info;
+int igb_discretization_info(const igb_discretization* d, igb_disc_info* out);
+/* local_to_global / local_sign (spaces.hpp:60-61): element_count*local_count each */
+int igb_discretization_l2g(const igb_discretization* d, int* l2g, double* sign);
+/* Element (spaces.hpp:15-21): ints[3*e] = patch, ix, iy; dbl[9*e] = h, ox, oy,
+ * box min xyz, box max xyz */
+int igb_discretization_elements(const igb_discretization* d, int* ints, double* dbl);
+/* classify_pair (spaces.hpp:67, spaces.cpp:309-394); maps = swap, flip_u,
+ * flip_v of map_a then map_b */
+int igb_classify_pair(const igb_discretization* d, int ea, int eb, int* cls, int maps[6]);
+void igb_discretization_destroy(igb_discretization* d);
+
+/* H2Options{m, eta, AssemblyOptions{far_order, sing_order}}  h2.hpp:11-15,
+ * assembly.hpp:13-20 (0 orders resolve to P+2 / P+3) */
+typedef struct {
+  int m;
+  double eta;
+  int far_order;
+  int sing_order;
+} igb_h2_opts;
+/* H2Storage (h2.hpp:49-53), reference convention: entries and bytes of the
+ * reference storage format (h2.cpp:380-390) */
+typedef struct {
+  size_t nearfield_entries, farfield_entries, total_bytes;
+} igb_h2_storage;
+
+/* H2Matrix<Scalar>(disc, opts)  h2.hpp:60, h2.cpp:99-129: full assembly on
+ * CUDA device `device`.  The discretization may be destroyed afterwards. */
+int igb_h2_create(const igb_discretization* d, const igb_h2_opts* opts, int device, igb_h2** out);
+/* rows()/cols()  h2.hpp:62-63 */
+int igb_h2_dim(const igb_h2* h, int* rows);
+/* apply(x) / operator*  h2.hpp:64-69, h2.cpp:254-378: host buffers of rows()
+ * scalars (double, or interleaved complex for Helmholtz/Maxwell) */
+int igb_h2_apply(igb_h2* h, const double* x, double* y);
+/* same with device pointers on `stream` (cudaStream_t, NULL = handle stream) */
+int igb_h2_apply_device(igb_h2* h, const double* x, double* y, void* stream);
+/* storage_report()  h2.hpp:71 */
+int igb_h2_storage_report(const igb_h2* h, igb_h2_storage* out);
+/* nearfield_pairs().size(), farfield_pairs().size(), tree().node_count() */
+int igb_h2_counts(const igb_h2* h, long long* n_near, long long* n_far, int* n_nodes);
+/* nearfield_pairs() / farfield_pairs()  h2.hpp:74-75: 2 ints per pair, sorted */
+int igb_h2_near_pairs(const igb_h2* h, int* out);
+int igb_h2_far_pairs(const igb_h2* h, int* out);
+/* tree() (ClusterTree, h2.hpp:25-47): per node patch, level, sx, sy and the
+ * box (min xyz, max xyz) */
+int igb_h2_tree(const igb_h2* h, int* patch, int* level, int* sx, int* sy, double* boxes);
+
+/* ---- introspection of the assembled operator (parity tests) ---- */
+/* near blocks of sorted near pairs [first, first+count): nl*nl scalars each,
+ * row-major [la][lb] (= NearBlock::blk, h2.hpp:86-89) */
+int igb_h2_near_blocks(const igb_h2* h, long long first, long long count, double* out);
+/* couplings of sorted far pairs: m^2*m^2 scalars each, column-major K(nu, mu)
+ * (= FarPair::coupling, h2.hpp:90-93) */
+int igb_h2_couplings(const igb_h2* h, long long first, long long count, double* out);
+/* moments per element: nl x (nch*m^2), [e][l][row], real (= moments_[e]^T,
+ * h2.hpp:101) */
+int igb_h2_moments(const igb_h2* h, double* out);
+/* interpolation-node images per node: m^2 x 3 (h2.cpp:182-196) */
+int igb_h2_images(const igb_h2* h, double* out);
+
+/* ---- measurement ---- */
+typedef struct {
+  double plan_host_ms, upload_ms, elements_ms, images_ms, couplings_ms, regular_ms, coincident_ms,
+      edge_ms, vertex_ms, device_total_ms, wall_total_ms;
+} igb_h2_times;
+int igb_h2_assembly_times(const igb_h2* h, igb_h2_times* out);
+/* bytes of the device-resident operator in this implementation's format */
+int igb_h2_device_bytes(const igb_h2* h, size_t* near, size_t* far, size_t* moments);
+/* `iters` back-to-back matvecs on device-resident buffers, CUDA-event timed;
+ * *launches = kernels per matvec */
+int igb_h2_bench_apply(igb_h2* h, int iters, float* ms, int* launches);
+void igb_h2_destroy(igb_h2* h);
+
+/* eta-admissibility of two boxes (min xyz, max xyz), h2.cpp:92-97 */
+int igb_admissible(const double box_a[6], const double box_b[6], double eta);
+int igb_last_error(char* buf, size_t n);
+int igb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IGABEM_B200_H */

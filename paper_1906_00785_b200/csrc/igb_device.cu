@@ -1,0 +1,1424 @@
+// B200 (sm_100a) kernels for the H² single-layer / EFIE operator:
+//   assembly  : element quadrature caches + Chebyshev moments (h2.cpp:131-173,
+//               pair_integration.hpp:40-73), interpolation-node images
+//               (h2.cpp:182-196), far couplings (h2.cpp:218-229), regular near
+//               blocks (pair_integration.hpp:76-95) and Sauter-Schwab singular
+//               blocks batched by class (pair_integration.hpp:98-148,
+//               quadrature.cpp:82-199);
+//   matvec    : the seven phases of H2Matrix::apply (h2.cpp:254-378).
+// All FP64.  Every reduction is a fixed-order loop (no atomics), so results
+// are bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "igb_device.hpp"
+
+#define IGB_CUDA(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" + \
+                               #x + ")");                                                    \
+  } while (0)
+
+namespace igb {
+namespace dev {
+
+constexpr double kInv4Pi = 0.079577471545947667884;  // 1 / (4 pi)
+constexpr int kCellStride = 104;                       // 100 coefficients + u0, v0 (+pad)
+
+// ------------------------------------------------------------ scalars
+struct __align__(16) cd {
+  double x, y;
+};
+__host__ __device__ __forceinline__ cd mk(double a, double b) {
+  cd r;
+  r.x = a;
+  r.y = b;
+  return r;
+}
+template <class S>
+__device__ __forceinline__ S zero();
+template <>
+__device__ __forceinline__ double zero<double>() { return 0.0; }
+template <>
+__device__ __forceinline__ cd zero<cd>() { return mk(0.0, 0.0); }
+
+__device__ __forceinline__ double operator_add(double a, double b) { return a + b; }
+__device__ __forceinline__ cd operator+(cd a, cd b) { return mk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cd operator*(cd a, cd b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ cd operator*(cd a, double b) { return mk(a.x * b, a.y * b); }
+__device__ __forceinline__ cd operator*(double b, cd a) { return mk(a.x * b, a.y * b); }
+
+__device__ __forceinline__ void fmac(double& acc, double a, double b) { acc = fma(a, b, acc); }
+__device__ __forceinline__ void fmac(cd& acc, cd a, double b) {
+  acc.x = fma(a.x, b, acc.x);
+  acc.y = fma(a.y, b, acc.y);
+}
+__device__ __forceinline__ void fmac(cd& acc, double a, cd b) { fmac(acc, b, a); }
+__device__ __forceinline__ void fmac(cd& acc, cd a, cd b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ double shfl_down(double v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ cd shfl_down(cd v, int o) {
+  return mk(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
+}
+__device__ __forceinline__ double shfl_idx(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ cd shfl_idx(cd v, int src) {
+  return mk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ double ldg_s(const double* p) { return __ldg(p); }
+__device__ __forceinline__ cd ldg_s(const cd* p) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  return mk(v.x, v.y);
+}
+template <class S>
+__device__ __forceinline__ S warp_sum(S v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = v + shfl_down(v, o);
+  return v;  // valid in lane 0
+}
+
+// ------------------------------------------------------ kernel traits
+struct KParams {
+  double kr, ki;      // wavenumber
+  double dwx, dwy;    // -1/kappa^2 (Maxwell divergence weight)
+};
+template <int Q_>
+struct LapT {
+  using S = double;
+  static constexpr int KIND = 0, Q = Q_, NL = (Q_ + 1) * (Q_ + 1), NC = 1, CHUNK = 128;
+  static constexpr int TS = Q_ + 1;                  // accumulation tile side
+  static constexpr int TABN = 2 * (Q_ + 1) * (Q_ + 1);  // per element: u and v tables
+};
+template <int Q_>
+struct HelmT {
+  using S = cd;
+  static constexpr int KIND = 1, Q = Q_, NL = (Q_ + 1) * (Q_ + 1), NC = 1, CHUNK = 128;
+  static constexpr int TS = Q_ + 1;
+  static constexpr int TABN = 2 * (Q_ + 1) * (Q_ + 1);
+};
+template <int P_>
+struct MaxT {
+  using S = cd;
+  static constexpr int KIND = 2, Q = P_, NL = 2 * (P_ + 1) * P_, NC = 4, CHUNK = 64;
+  static constexpr int TS = (NL % 4 == 0) ? 4 : 2;
+  // per element: p-tables (u, v) of (P+1)^2 and q-tables (u, v) of P^2, padded even
+  static constexpr int TABN = ((2 * (P_ + 1) * (P_ + 1) + 2 * P_ * P_) + 1) / 2 * 2;
+};
+
+// Green's functions (operators.hpp:16-20), distance clamped as in
+// pair_integration.hpp:18,118
+__device__ __forceinline__ double green(double r2, const KParams&, double) {
+  double rinv = rsqrt(r2);
+  if (r2 < 1e-28) rinv = 1e14;
+  return rinv * kInv4Pi;
+}
+__device__ __forceinline__ cd green_c(double r2, const KParams& kp) {
+  double r = sqrt(r2);
+  r = fmax(r, 1e-14);
+  double s, c;
+  sincos(kp.kr * r, &s, &c);
+  double a = kInv4Pi / r;
+  if (kp.ki != 0.0) a *= exp(kp.ki * r);
+  return mk(a * c, -a * s);
+}
+template <class KT>
+__device__ __forceinline__ typename KT::S green_k(double r2, const KParams& kp) {
+  if constexpr (KT::KIND == 0)
+    return green(r2, kp, 0.0);
+  else
+    return green_c(r2, kp);
+}
+
+// -------------------------------------------------------- geometry jet
+// cf: [c][j][i] (stride 5 / 25), homogeneous (wx, wy, wz, w) in (s, t)
+template <int D>
+__device__ __forceinline__ void jet(const double* __restrict__ cf, double s, double t, double x[3],
+                                    double du[3], double dv[3]) {
+  double N[4], Ns[4], Nt[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* p = cf + c * 25;
+    double n = 0.0, ns = 0.0, nt = 0.0;
+#pragma unroll
+    for (int j = D; j >= 0; --j) {
+      double r = p[j * 5 + D], rp = 0.0;
+#pragma unroll
+      for (int i = D - 1; i >= 0; --i) {
+        rp = fma(rp, s, r);
+        r = fma(r, s, p[j * 5 + i]);
+      }
+      nt = fma(nt, t, n);
+      n = fma(n, t, r);
+      ns = fma(ns, t, rp);
+    }
+    N[c] = n;
+    Ns[c] = ns;
+    Nt[c] = nt;
+  }
+  const double iw = 1.0 / N[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    x[k] = N[k] * iw;
+    du[k] = (Ns[k] - x[k] * Ns[3]) * iw;
+    dv[k] = (Nt[k] - x[k] * Nt[3]) * iw;
+  }
+}
+template <int D>
+__device__ __forceinline__ void point_only(const double* __restrict__ cf, double s, double t, double x[3]) {
+  double N[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* p = cf + c * 25;
+    double n = 0.0;
+#pragma unroll
+    for (int j = D; j >= 0; --j) {
+      double r = p[j * 5 + D];
+#pragma unroll
+      for (int i = D - 1; i >= 0; --i) r = fma(r, s, p[j * 5 + i]);
+      n = fma(n, t, r);
+    }
+    N[c] = n;
+  }
+  const double iw = 1.0 / N[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) x[k] = N[k] * iw;
+}
+__device__ __forceinline__ double sqrt_g_of(const double du[3], const double dv[3]) {
+  const double n0 = du[1] * dv[2] - du[2] * dv[1];
+  const double n1 = du[2] * dv[0] - du[0] * dv[2];
+  const double n2 = du[0] * dv[1] - du[1] * dv[0];
+  return sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+}
+
+// polynomial of degree DEG with coefficients c[0..DEG]
+template <int DEG>
+__device__ __forceinline__ double horner(const double* c, double s) {
+  double r = c[DEG];
+#pragma unroll
+  for (int k = DEG - 1; k >= 0; --k) r = fma(r, s, c[k]);
+  return r;
+}
+template <int DEG>
+__device__ __forceinline__ double horner_d(const double* c, double s) {
+  if constexpr (DEG == 0) {
+    return 0.0;
+  } else {
+    double r = DEG * c[DEG];
+#pragma unroll
+    for (int k = DEG - 1; k >= 1; --k) r = fma(r, s, k * c[k]);
+    return r;
+  }
+}
+
+// shape data of one point: NC channels x NL values (real).
+// scalar: value; Maxwell: field x/y/z and surface divergence
+// (spaces.cpp:257-307).  tab: element tables in smem.
+template <class KT>
+__device__ __forceinline__ void shapes(const double* __restrict__ tab, double s, double t, double h,
+                                       const double du[3], const double dv[3], double sg,
+                                       double out[KT::NC][KT::NL]) {
+  if constexpr (KT::KIND != 2) {
+    constexpr int Q = KT::Q;
+    double bu[Q + 1], bv[Q + 1];
+#pragma unroll
+    for (int i = 0; i <= Q; ++i) {
+      bu[i] = horner<Q>(tab + i * (Q + 1), s);
+      bv[i] = horner<Q>(tab + (Q + 1) * (Q + 1) + i * (Q + 1), t);
+    }
+#pragma unroll
+    for (int j = 0; j <= Q; ++j)
+#pragma unroll
+      for (int i = 0; i <= Q; ++i) out[0][i + (Q + 1) * j] = bu[i] * bv[j];
+  } else {
+    constexpr int P = KT::Q;
+    const double* tpu = tab;
+    const double* tpv = tab + (P + 1) * (P + 1);
+    const double* tqu = tab + 2 * (P + 1) * (P + 1);
+    const double* tqv = tqu + P * P;
+    double bpu[P + 1], bpv[P + 1], dpu[P + 1], dpv[P + 1], bqu[P], bqv[P];
+    const double ih = 1.0 / h;
+#pragma unroll
+    for (int i = 0; i <= P; ++i) {
+      bpu[i] = horner<P>(tpu + i * (P + 1), s);
+      bpv[i] = horner<P>(tpv + i * (P + 1), t);
+      dpu[i] = horner_d<P>(tpu + i * (P + 1), s) * ih;
+      dpv[i] = horner_d<P>(tpv + i * (P + 1), t) * ih;
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      bqu[i] = horner<P - 1>(tqu + i * P, s);
+      bqv[i] = horner<P - 1>(tqv + i * P, t);
+    }
+    const double ig = 1.0 / sg;
+    int l = 0;
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+#pragma unroll
+      for (int i = 0; i <= P; ++i, ++l) {
+        const double b = bpu[i] * bqv[j];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) out[k][l] = ig * du[k] * b;
+        out[3][l] = ig * dpu[i] * bqv[j];
+      }
+#pragma unroll
+    for (int j = 0; j <= P; ++j)
+#pragma unroll
+      for (int i = 0; i < P; ++i, ++l) {
+        const double b = bqu[i] * bpv[j];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) out[k][l] = ig * dv[k] * b;
+        out[3][l] = ig * bqu[i] * dpv[j];
+      }
+  }
+}
+
+// element tables (u, v) for grid position (ix, iy) into smem
+template <class KT>
+__device__ __forceinline__ void load_tables(double* dst, const double* __restrict__ ta,
+                                            const double* __restrict__ tb, int ix, int iy, int tid,
+                                            int nthreads) {
+  if constexpr (KT::KIND != 2) {
+    constexpr int T = (KT::Q + 1) * (KT::Q + 1);
+    for (int i = tid; i < 2 * T; i += nthreads) dst[i] = (i < T) ? ta[ix * T + i] : ta[iy * T + i - T];
+  } else {
+    constexpr int P = KT::Q, TP = (P + 1) * (P + 1), TQ = P * P;
+    for (int i = tid; i < 2 * TP + 2 * TQ; i += nthreads) {
+      double v;
+      if (i < TP) v = ta[ix * TP + i];
+      else if (i < 2 * TP) v = ta[iy * TP + i - TP];
+      else if (i < 2 * TP + TQ) v = tb[ix * TQ + i - 2 * TP];
+      else v = tb[iy * TQ + i - 2 * TP - TQ];
+      dst[i] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------ device args
+struct GeoArgs {
+  const double* cells;   // [cell][kCellStride]
+  const int* el_cell;
+  const double* tab_a;
+  const double* tab_b;
+  int level, epp;
+  double h;
+  KParams kp;
+};
+
+// offset (in scalars) of entry (la, lb) of near slot q in the row layout
+__device__ __forceinline__ size_t near_off(const int* __restrict__ near_a, const int* __restrict__ near_rs, int q,
+                                           int la, int lb, int NL) {
+  const int e = near_a[q];
+  const int rs = near_rs[e];
+  const int cnt = near_rs[e + 1] - rs;
+  return static_cast<size_t>(rs) * NL * NL + (static_cast<size_t>(la) * cnt + (q - rs)) * NL + lb;
+}
+
+// ---------------------------------------------------- K1: element caches
+// Per element: quadrature points, weighted shapes (far caches,
+// pair_integration.hpp:40-73) and Chebyshev moments (h2.cpp:131-173).
+template <class KT>
+__global__ void __launch_bounds__(128) k_element(GeoArgs g, int nf, const double* __restrict__ gx,
+                                                 const double* __restrict__ gw, int m,
+                                                 const double* __restrict__ lag,  // [m][nf]
+                                                 double* __restrict__ cpts, double* __restrict__ cval,
+                                                 double* __restrict__ mom) {
+  constexpr int NL = KT::NL, NC = KT::NC;
+  extern __shared__ __align__(16) double sm[];
+  double* cf = sm;
+  double* tab = sm + 104;
+  double* wphi = tab + KT::TABN;  // [nq][NC*NL]
+  const int e = blockIdx.x, tid = threadIdx.x;
+  const int cell = g.el_cell[e];
+  const int r = e % g.epp, n1 = 1 << g.level, ix = r % n1, iy = r / n1;
+  for (int i = tid; i < 100; i += blockDim.x) cf[i] = g.cells[static_cast<size_t>(cell) * kCellStride + i];
+  load_tables<KT>(tab, g.tab_a, g.tab_b, ix, iy, tid, blockDim.x);
+  __syncthreads();
+  const double u0 = g.cells[static_cast<size_t>(cell) * kCellStride + 100];
+  const double v0 = g.cells[static_cast<size_t>(cell) * kCellStride + 101];
+  const double ox = ix * g.h, oy = iy * g.h;
+  const int nq = nf * nf;
+  for (int q = tid; q < nq; q += blockDim.x) {
+    const int a = q % nf, b = q / nf;
+    const double ul = gx[a], vl = gx[b];
+    double x[3], du[3], dv[3];
+    jet<4>(cf, ox + g.h * ul - u0, oy + g.h * vl - v0, x, du, dv);
+    const double sg = sqrt_g_of(du, dv);
+    const double w = gw[a] * gw[b] * sg * g.h * g.h;
+    double sh[NC][NL];
+    shapes<KT>(tab, ul, vl, g.h, du, dv, sg, sh);
+    for (int k = 0; k < 3; ++k) cpts[(static_cast<size_t>(e) * nq + q) * 3 + k] = x[k];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const double v = w * sh[c][l];
+        cval[((static_cast<size_t>(e) * NC + c) * nq + q) * NL + l] = v;
+        wphi[q * (NC * NL) + c * NL + l] = v;
+      }
+  }
+  __syncthreads();
+  const int mm = m * m, rows = NC * mm;
+  for (int o = tid; o < NL * rows; o += blockDim.x) {
+    const int l = o / rows, rr = o % rows, c = rr / mm, nu = rr % mm, iu = nu % m, iv = nu / m;
+    double acc = 0.0;
+    for (int b = 0; b < nf; ++b) {
+      double in = 0.0;
+      for (int a = 0; a < nf; ++a) in = fma(lag[iu * nf + a], wphi[(a + nf * b) * (NC * NL) + c * NL + l], in);
+      acc = fma(lag[iv * nf + b], in, acc);
+    }
+    mom[(static_cast<size_t>(e) * NL + l) * rows + rr] = acc;
+  }
+}
+
+// --------------------------------------------------------- K2: images
+struct PatchDev {
+  const int* info;      // per patch: cell_base, pu, pv, nku, nkv, ku_off, kv_off
+  const double* knots;
+};
+__device__ __forceinline__ int find_span_dev(const double* k, int p, int nk, double x) {  // splines.cpp:20-38
+  const int n = nk - p - 1;
+  if (x >= k[n]) {
+    int j = n - 1;
+    while (k[j + 1] <= k[j]) --j;
+    return j;
+  }
+  int lo = p, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (x < k[mid]) hi = mid;
+    else lo = mid;
+  }
+  return lo;
+}
+__global__ void k_images(int n_nodes, int m, const double* __restrict__ cheb, const int* __restrict__ node_patch,
+                         const int* __restrict__ node_level, const int* __restrict__ node_sx,
+                         const int* __restrict__ node_sy, PatchDev pd, const double* __restrict__ cells,
+                         double* __restrict__ img) {
+  const int mm = m * m;
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n_nodes) * mm) return;
+  const int node = static_cast<int>(idx / mm), nu = static_cast<int>(idx % mm), iu = nu % m, iv = nu / m;
+  const int p = node_patch[node];
+  const double hs = 1.0 / (1 << node_level[node]);
+  const double u = hs * (node_sx[node] + cheb[iu]);
+  const double v = hs * (node_sy[node] + cheb[iv]);
+  const int* inf = pd.info + 7 * p;
+  const int su = find_span_dev(pd.knots + inf[5], inf[1], inf[3], u);
+  const int sv = find_span_dev(pd.knots + inf[6], inf[2], inf[4], v);
+  const int nsv = (inf[4] - inf[2] - 1) - inf[2];
+  const int cell = inf[0] + (su - inf[1]) * nsv + (sv - inf[2]);
+  const double* cf = cells + static_cast<size_t>(cell) * kCellStride;
+  double x[3];
+  point_only<4>(cf, u - cf[100], v - cf[101], x);
+  for (int k = 0; k < 3; ++k) img[idx * 3 + k] = x[k];
+}
+
+// ------------------------------------------------------ K3: couplings
+// K[q][mu][nu] = G(|img_ta[nu] - img_tb[mu]|)  (h2.cpp:218-229)
+template <class KT>
+__global__ void __launch_bounds__(256) k_couplings(long long n_pairs, int mm, const int* __restrict__ far_a,
+                                                   const int* __restrict__ far_b, const double* __restrict__ img,
+                                                   KParams kp, double* __restrict__ out) {
+  using S = typename KT::S;
+  S* K = reinterpret_cast<S*>(out);
+  const long long mm2 = static_cast<long long>(mm) * mm;
+  const long long total = n_pairs * mm2;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long q = i / mm2;
+    const int r = static_cast<int>(i % mm2), nu = r % mm, mu = r / mm;
+    const double* a = img + (static_cast<size_t>(far_a[q]) * mm + nu) * 3;
+    const double* b = img + (static_cast<size_t>(far_b[q]) * mm + mu) * 3;
+    const double d0 = a[0] - b[0], d1 = a[1] - b[1], d2 = a[2] - b[2];
+    K[i] = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+  }
+}
+
+// --------------------------------------------------- K4: regular near
+// blk = sum_c w_c A_c^T (K B_c)  (pair_integration.hpp:76-95)
+template <class KT>
+__global__ void __launch_bounds__(128) k_regular(const int* __restrict__ slots, const int* __restrict__ near_a,
+                                                 const int* __restrict__ near_b, const int* __restrict__ near_rs,
+                                                 int nq, const double* __restrict__ cpts,
+                                                 const double* __restrict__ cval, KParams kp,
+                                                 double* __restrict__ near) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL, NC = KT::NC;
+  extern __shared__ __align__(16) double sm[];
+  S* KB = reinterpret_cast<S*>(sm);  // [NC][nq][NL]
+  const int q = slots[blockIdx.x];
+  const int ea = near_a[q], eb = near_b[q];
+  const double* pa = cpts + static_cast<size_t>(ea) * nq * 3;
+  const double* pb = cpts + static_cast<size_t>(eb) * nq * 3;
+  for (int it = threadIdx.x; it < nq * NC; it += blockDim.x) {
+    const int i = it % nq, c = it / nq;
+    const double xa = pa[3 * i], ya = pa[3 * i + 1], za = pa[3 * i + 2];
+    const double* B = cval + (static_cast<size_t>(eb) * NC + c) * nq * NL;
+    S acc[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = zero<S>();
+    for (int j = 0; j < nq; ++j) {
+      const double d0 = xa - pb[3 * j], d1 = ya - pb[3 * j + 1], d2 = za - pb[3 * j + 2];
+      const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) fmac(acc[l], gk, B[j * NL + l]);
+    }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) KB[(c * nq + i) * NL + l] = acc[l];
+  }
+  __syncthreads();
+  S* out = reinterpret_cast<S*>(near);
+  for (int o = threadIdx.x; o < NL * NL; o += blockDim.x) {
+    const int la = o / NL, lb = o % NL;
+    S tot = zero<S>();
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double* A = cval + (static_cast<size_t>(ea) * NC + c) * nq * NL;
+      S s = zero<S>();
+      for (int i = 0; i < nq; ++i) fmac(s, KB[(c * nq + i) * NL + lb], A[i * NL + la]);
+      if constexpr (KT::KIND == 2) {
+        if (c == 3) s = s * mk(kp.dwx, kp.dwy);
+      }
+      tot = tot + s;
+    }
+    out[near_off(near_a, near_rs, q, la, lb, NL)] = tot;
+  }
+}
+
+// ---------------------------------------------------- K5: singular near
+// Regularised relative-coordinate rules generated in-register
+// (quadrature.cpp:82-177); one CTA per unique pair (ea <= eb), the block and
+// its transpose written to both ordered slots (pair_integration.hpp:139-148).
+template <int CLS>
+__device__ __forceinline__ void rule_point(int p, int n, const double* gx, const double* gw, double& ua,
+                                           double& va, double& ub, double& vb, double& w) {
+  const int i4 = p % n;
+  p /= n;
+  const int i3 = p % n;
+  p /= n;
+  const int i2 = p % n;
+  p /= n;
+  const int i1 = p % n;
+  const int sec = p / n;
+  const double wp = gw[i1] * gw[i2] * gw[i3] * gw[i4];
+  if constexpr (CLS == 3) {  // coincident (quadrature.cpp:82-111)
+    const int axis = sec >> 2;
+    const double dir = (sec & 2) ? -1.0 : 1.0, sgn = (sec & 1) ? -1.0 : 1.0;
+    const double t = gx[i1], s = gx[i2];
+    double z1, z2;
+    if (axis == 0) {
+      z1 = dir * t;
+      z2 = sgn * t * s;
+    } else {
+      z1 = sgn * t * s;
+      z2 = dir * t;
+    }
+    const double lx = 1.0 - fabs(z1), ly = 1.0 - fabs(z2);
+    const double x1 = fmax(0.0, -z1) + lx * gx[i3];
+    const double x2 = fmax(0.0, -z2) + ly * gx[i4];
+    ua = x1;
+    va = x2;
+    ub = x1 + z1;
+    vb = x2 + z2;
+    w = wp * t * lx * ly;
+  } else if constexpr (CLS == 2) {  // edge (quadrature.cpp:113-149)
+    const int kind = sec >> 1;
+    const double sgn = (sec & 1) ? -1.0 : 1.0;
+    const double t = gx[i1], a = gx[i2], b = gx[i3];
+    double d, jac;
+    if (kind == 0) {
+      va = t; vb = t * b; d = sgn * t * a; jac = t * t * (1.0 - t * a);
+    } else if (kind == 1) {
+      vb = t; va = t * b; d = sgn * t * a; jac = t * t * (1.0 - t * a);
+    } else {
+      d = sgn * t; va = t * a; vb = t * b; jac = t * t * (1.0 - t);
+    }
+    ua = fmax(0.0, -d) + (1.0 - fabs(d)) * gx[i4];
+    ub = ua + d;
+    w = wp * jac;
+  } else {  // vertex (quadrature.cpp:151-177)
+    const double t = gx[i1];
+    const double v1 = t * gx[i2], v2 = t * gx[i3], v3 = t * gx[i4];
+    switch (sec) {
+      case 0: ua = t; va = v1; ub = v2; vb = v3; break;
+      case 1: ua = v1; va = t; ub = v2; vb = v3; break;
+      case 2: ua = v1; va = v2; ub = t; vb = v3; break;
+      default: ua = v1; va = v2; ub = v3; vb = t; break;
+    }
+    w = wp * t * t * t;
+  }
+}
+__device__ __forceinline__ void apply_map(int bits, double& u, double& v) {  // quadrature.hpp:25-29
+  if (bits & 1) {
+    const double t = u;
+    u = v;
+    v = t;
+  }
+  if (bits & 2) u = 1.0 - u;
+  if (bits & 4) v = 1.0 - v;
+}
+
+struct SingArgs {
+  int n_pairs, n;
+  const int *ea, *eb, *slot_ab, *slot_ba;
+  const unsigned char *map_a, *map_b;
+  const double *gx, *gw;
+  const int *near_a, *near_rs;
+  double* near;
+};
+
+template <class KT>
+struct SingLayout {
+  static constexpr int NL = KT::NL, NC = KT::NC, CH = KT::CHUNK, TS = KT::TS;
+  static constexpr int NTR = NL / TS, NT = NTR * NTR, SL = 128 / NT;
+  static constexpr int STR = ((NC * NL) % 2 == 0) ? NC * NL + 1 : NC * NL;
+  static constexpr int SW = sizeof(typename KT::S) / 8;
+  static constexpr int HEAD = 104 * 2 + 2 * KT::TABN + 128;
+  static constexpr int STAGE = CH * STR * (SW + 1);
+  static constexpr int RED = SL * NL * NL * SW;
+  static constexpr int BODY = STAGE > RED ? STAGE : RED;
+  static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY) * 8;
+  static_assert(NL % TS == 0, "tile");
+  static_assert(NT <= 128, "tiles");
+};
+
+template <class KT, int CLS>
+__global__ void __launch_bounds__(128) k_singular(GeoArgs g, SingArgs A) {
+  using S = typename KT::S;
+  using LY = SingLayout<KT>;
+  constexpr int NL = KT::NL, NC = KT::NC, CH = LY::CH, TS = LY::TS, NTR = LY::NTR, NT = LY::NT,
+                SL = LY::SL, STR = LY::STR;
+  extern __shared__ __align__(16) double sm[];
+  double* cfa = sm;
+  double* cfb = sm + 104;
+  double* taba = sm + 208;
+  double* tabb = taba + KT::TABN;
+  double* gx = tabb + KT::TABN;
+  double* gw = gx + 64;
+  double* body = gw + 64;
+  S* Ga = reinterpret_cast<S*>(body);
+  double* Fb = body + CH * STR * LY::SW;
+
+  const int tid = threadIdx.x;
+  const int pr = blockIdx.x;
+  const int ea = A.ea[pr], eb = A.eb[pr];
+  const int ma = A.map_a[pr], mb = A.map_b[pr];
+  const int cella = g.el_cell[ea], cellb = g.el_cell[eb];
+  const int n1 = 1 << g.level;
+  const int ra = ea % g.epp, rb = eb % g.epp;
+  const int ixa = ra % n1, iya = ra / n1, ixb = rb % n1, iyb = rb / n1;
+  for (int i = tid; i < 104; i += 128) {
+    cfa[i] = g.cells[static_cast<size_t>(cella) * kCellStride + i];
+    cfb[i] = g.cells[static_cast<size_t>(cellb) * kCellStride + i];
+  }
+  load_tables<KT>(taba, g.tab_a, g.tab_b, ixa, iya, tid, 128);
+  load_tables<KT>(tabb, g.tab_a, g.tab_b, ixb, iyb, tid, 128);
+  const int n = A.n;
+  if (tid < n) {
+    gx[tid] = A.gx[tid];
+    gw[tid] = A.gw[tid];
+  }
+  __syncthreads();
+  const double h = g.h;
+  const double sxa = ixa * h - cfa[100], sya = iya * h - cfa[101];
+  const double sxb = ixb * h - cfb[100], syb = iyb * h - cfb[101];
+  const double h4 = h * h * h * h;
+  const int n4 = n * n * n * n;
+  const int npts = (CLS == 3 ? 8 : (CLS == 2 ? 6 : 4)) * n4;
+
+  S acc[TS][TS];
+#pragma unroll
+  for (int i = 0; i < TS; ++i)
+#pragma unroll
+    for (int j = 0; j < TS; ++j) acc[i][j] = zero<S>();
+  const int tile = tid % NT, slice = tid / NT;
+  const int tr = (tile / NTR) * TS, tc = (tile % NTR) * TS;
+  const bool active = slice < SL;
+
+  for (int base = 0; base < npts; base += CH) {
+    if (tid < CH) {
+      const int p = base + tid;
+      S* ga = Ga + tid * STR;
+      double* fb = Fb + tid * STR;
+      if (p < npts) {
+        double ua, va, ub, vb, w;
+        rule_point<CLS>(p, n, gx, gw, ua, va, ub, vb, w);
+        apply_map(ma, ua, va);
+        apply_map(mb, ub, vb);
+        double xa[3], dua[3], dva[3], xb[3], dub[3], dvb[3];
+        jet<4>(cfa, sxa + h * ua, sya + h * va, xa, dua, dva);
+        jet<4>(cfb, sxb + h * ub, syb + h * vb, xb, dub, dvb);
+        const double sga = sqrt_g_of(dua, dva), sgb = sqrt_g_of(dub, dvb);
+        const double d0 = xa[0] - xb[0], d1 = xa[1] - xb[1], d2 = xa[2] - xb[2];
+        const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, g.kp);
+        const double wt = w * sga * sgb * h4;
+        const S gwt = gk * wt;
+        double sa[NC][NL], sb[NC][NL];
+        shapes<KT>(taba, ua, va, h, dua, dva, sga, sa);
+        shapes<KT>(tabb, ub, vb, h, dub, dvb, sgb, sb);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          S wc = gwt;
+          if constexpr (KT::KIND == 2) {
+            if (c == 3) wc = gwt * mk(g.kp.dwx, g.kp.dwy);
+          }
+#pragma unroll
+          for (int l = 0; l < NL; ++l) {
+            ga[c * NL + l] = wc * sa[c][l];
+            fb[c * NL + l] = sb[c][l];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC * NL; ++c) {
+          ga[c] = zero<S>();
+          fb[c] = 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    if (active) {
+      for (int pt = slice; pt < CH; pt += SL) {
+        const S* ga = Ga + pt * STR;
+        const double* fb = Fb + pt * STR;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          S av[TS];
+          double bv[TS];
+#pragma unroll
+          for (int i = 0; i < TS; ++i) {
+            av[i] = ga[c * NL + tr + i];
+            bv[i] = fb[c * NL + tc + i];
+          }
+#pragma unroll
+          for (int i = 0; i < TS; ++i)
+#pragma unroll
+            for (int j = 0; j < TS; ++j) fmac(acc[i][j], av[i], bv[j]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  S* red = reinterpret_cast<S*>(body);
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < TS; ++i)
+#pragma unroll
+      for (int j = 0; j < TS; ++j) red[(slice * NL + tr + i) * NL + tc + j] = acc[i][j];
+  }
+  __syncthreads();
+  S* out = reinterpret_cast<S*>(A.near);
+  const int qab = A.slot_ab[pr], qba = A.slot_ba[pr];
+  for (int o = tid; o < NL * NL; o += 128) {
+    S v = zero<S>();
+    for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + o];
+    const int la = o / NL, lb = o % NL;
+    out[near_off(A.near_a, A.near_rs, qab, la, lb, NL)] = v;
+    if (qba != qab) out[near_off(A.near_a, A.near_rs, qba, lb, la, NL)] = v;
+  }
+}
+
+// --------------------------------------------------------- K6: matvec
+template <class S>
+__global__ void k_coef(int n, const S* __restrict__ x, const int* __restrict__ l2g, const double* __restrict__ sg,
+                       S* __restrict__ coef) {  // h2.cpp:271-279
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) coef[i] = x[l2g[i]] * sg[i];
+}
+__device__ __forceinline__ double operator_mul(double a, double b) { return a * b; }
+
+template <class S>
+__global__ void k_leaf_up(int ne, int nl, int rows, int epp, int npp, int leaf_off, const double* __restrict__ mom,
+                          const S* __restrict__ coef, S* __restrict__ up) {  // h2.cpp:281-290
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(ne) * rows) return;
+  const int e = static_cast<int>(idx / rows), r = static_cast<int>(idx % rows);
+  S acc = zero<S>();
+  for (int l = 0; l < nl; ++l) fmac(acc, coef[static_cast<size_t>(e) * nl + l], mom[(static_cast<size_t>(e) * nl + l) * rows + r]);
+  const int leaf = (e / epp) * npp + leaf_off + (e % epp);
+  up[static_cast<size_t>(leaf) * rows + r] = acc;
+}
+
+// parent(i,j) = sum_k tu_k X_k tv_k^T  (h2.cpp:291-310)
+template <class S>
+__global__ void k_up_level(int np, int level, int npp, int off_l, int off_c, int m, int nch,
+                           const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ up) {
+  const int mm = m * m, rows = nch * mm, nside = 1 << level, per = nside * nside;
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(np) * per * rows) return;
+  const int r = static_cast<int>(idx % rows);
+  const long long nidx = idx / rows;
+  const int p = static_cast<int>(nidx / per), s = static_cast<int>(nidx % per);
+  const int sx = s % nside, sy = s / nside, c = r / mm, nu = r % mm, i = nu % m, j = nu / m;
+  const int cside = nside * 2;
+  S acc = zero<S>();
+  for (int k = 0; k < 4; ++k) {
+    const int child = p * npp + off_c + (2 * sx + (k & 1)) + cside * (2 * sy + (k >> 1));
+    const double* tu = (k & 1) ? tr : tl;
+    const double* tv = (k >> 1) ? tr : tl;
+    const S* X = up + static_cast<size_t>(child) * rows + c * mm;
+    for (int b = 0; b < m; ++b) {
+      S t = zero<S>();
+      for (int a = 0; a < m; ++a) fmac(t, X[a + m * b], tu[i + m * a]);
+      fmac(acc, t, tv[j + m * b]);
+    }
+  }
+  up[static_cast<size_t>(p * npp + off_l + s) * rows + r] = acc;
+}
+
+// down[t] = sum_q w_c K_q up[tb_q]  (h2.cpp:312-326); one warp per target
+template <class S, int NCH, int R>
+__global__ void __launch_bounds__(256) k_far(int n_targets, const int* __restrict__ targets,
+                                             const int* __restrict__ far_rs, const int* __restrict__ far_b,
+                                             const S* __restrict__ K, int mm, const S* __restrict__ up,
+                                             S dw, S* __restrict__ down) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_targets) return;
+  const int t = targets[warp];
+  const int rows = NCH * mm;
+  const int G = (mm <= 32) ? 32 / mm : 1;
+  const int g = (mm <= 32) ? lane / mm : 0;
+  const int nu0 = (mm <= 32) ? lane % mm : lane;
+  const bool ok = g < G;
+  S acc[NCH][R];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[c][r] = zero<S>();
+  const int q0 = far_rs[t], q1 = far_rs[t + 1];
+  if (ok) {
+    for (int q = q0 + g; q < q1; q += G) {
+      const S* Kq = K + static_cast<size_t>(q) * mm * mm;
+      const S* src = up + static_cast<size_t>(far_b[q]) * rows;
+      S part[NCH][R];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int r = 0; r < R; ++r) part[c][r] = zero<S>();
+#pragma unroll 4
+      for (int mu = 0; mu < mm; ++mu) {
+        S xv[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) xv[c] = src[c * mm + mu];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int nu = nu0 + 32 * r;
+          if (nu < mm) {
+            const S kv = ldg_s(Kq + mu * mm + nu);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) fmac(part[c][r], kv, xv[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (NCH == 4 && c == 3)
+            acc[c][r] = acc[c][r] + part[c][r] * dw;
+          else
+            acc[c][r] = acc[c][r] + part[c][r];
+        }
+    }
+  }
+  // combine the G lane groups in fixed order
+  for (int gg = 1; gg < G; ++gg) {
+    const int src = (lane + gg * mm < 32) ? lane + gg * mm : lane;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const S v = shfl_idx(acc[c][0], src);
+      if (g == 0) acc[c][0] = acc[c][0] + v;
+    }
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int nu = nu0 + 32 * r;
+      if (nu < mm)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) down[static_cast<size_t>(t) * rows + c * mm + nu] = acc[c][r];
+    }
+  }
+}
+
+// child(i,j) += tu^T X tv  (h2.cpp:328-347)
+template <class S>
+__global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, int m, int nch,
+                             const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ down) {
+  const int mm = m * m, rows = nch * mm, cside = 2 << level, per = cside * cside;
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(np) * per * rows) return;
+  const int r = static_cast<int>(idx % rows);
+  const long long nidx = idx / rows;
+  const int p = static_cast<int>(nidx / per), s = static_cast<int>(nidx % per);
+  const int sx = s % cside, sy = s / cside, c = r / mm, nu = r % mm, i = nu % m, j = nu / m;
+  const int parent = p * npp + off_p + (sx / 2) + (cside / 2) * (sy / 2);
+  const double* tu = (sx & 1) ? tr : tl;
+  const double* tv = (sy & 1) ? tr : tl;
+  const S* X = down + static_cast<size_t>(parent) * rows + c * mm;
+  S acc = zero<S>();
+  for (int b = 0; b < m; ++b) {
+    S t = zero<S>();
+    for (int a = 0; a < m; ++a) fmac(t, X[a + m * b], tu[a + m * i]);
+    fmac(acc, t, tv[b + m * j]);
+  }
+  S* Y = down + static_cast<size_t>(p * npp + off_c + s) * rows + c * mm;
+  Y[nu] = Y[nu] + acc;
+}
+
+// near rows + leaf backward transform per element (h2.cpp:349-376); one warp
+template <class S, int NL>
+__global__ void __launch_bounds__(256) k_near_leaf(int ne, const int* __restrict__ near_rs,
+                                                   const int* __restrict__ near_b, const S* __restrict__ blk,
+                                                   const S* __restrict__ coef, int rows, int epp, int npp,
+                                                   int leaf_off, const double* __restrict__ mom,
+                                                   const S* __restrict__ down, S* __restrict__ loc) {
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= ne) return;
+  const int rs = near_rs[e], cnt = near_rs[e + 1] - rs;
+  const int len = cnt * NL;
+  const S* base = blk + static_cast<size_t>(rs) * NL * NL;
+  S acc[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) acc[l] = zero<S>();
+  for (int j = lane; j < len; j += 32) {
+    const int k = j / NL, lb = j - k * NL;
+    const S xv = coef[static_cast<size_t>(near_b[rs + k]) * NL + lb];
+#pragma unroll
+    for (int la = 0; la < NL; ++la) fmac(acc[la], base[static_cast<size_t>(la) * len + j], xv);
+  }
+  const int leaf = (e / epp) * npp + leaf_off + (e % epp);
+  const S* dn = down + static_cast<size_t>(leaf) * rows;
+  S lf[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    S s = zero<S>();
+    const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
+    for (int r = lane; r < rows; r += 32) fmac(s, dn[r], mc[r]);
+    lf[l] = s;
+  }
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const S a = warp_sum(acc[l]);
+    const S b = warp_sum(lf[l]);
+    if (lane == 0) loc[static_cast<size_t>(e) * NL + l] = a + b;
+  }
+}
+
+template <class S>
+__global__ void k_scatter(int nd, const int* __restrict__ start, const int* __restrict__ inc,
+                          const double* __restrict__ sg, const S* __restrict__ loc, S* __restrict__ y) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= nd) return;
+  S acc = zero<S>();
+  for (int i = start[d]; i < start[d + 1]; ++i) {
+    const int k = inc[i];
+    acc = acc + loc[k] * sg[k];
+  }
+  y[d] = acc;
+}
+
+template <class S>
+__global__ void k_zero(size_t n, S* p) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = zero<S>();
+}
+
+}  // namespace dev
+
+// ====================================================== host driver
+using namespace dev;
+
+template <class T>
+T* H2Device::dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  IGB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  allocs_.push_back(p);
+  return static_cast<T*>(p);
+}
+template <class T>
+T* H2Device::upload(const std::vector<T>& v) {
+  T* p = dalloc<T>(v.size());
+  if (!v.empty()) IGB_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream_));
+  return p;
+}
+
+static unsigned grid_for(long long n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
+
+H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, int far_order, int sing_order,
+                   int device, int flags)
+    : disc_(std::move(d)), device_(device), flags_(flags) {
+  const auto t_wall0 = std::chrono::steady_clock::now();
+  int ndev = 0;
+  IGB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) throw std::invalid_argument("H2Matrix: CUDA device index out of range");
+  IGB_CUDA(cudaSetDevice(device_));
+  IGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  const auto t0 = std::chrono::steady_clock::now();
+  plan_ = build_plan(*disc_, m, eta, far_order, sing_order);
+  times_.plan_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  nch_ = disc_->is_vector() ? 4 : 1;
+  const int kind = disc_->kind();
+  const int q = disc_->kind() == kMaxwell ? disc_->degree() : disc_->scalar_degree();
+  try {
+    if (kind == kLaplace) {
+      switch (q) {
+        case 0: assemble_impl<LapT<0>>(); break;
+        case 1: assemble_impl<LapT<1>>(); break;
+        case 2: assemble_impl<LapT<2>>(); break;
+        case 3: assemble_impl<LapT<3>>(); break;
+        case 4: assemble_impl<LapT<4>>(); break;
+        default: throw std::invalid_argument("B200 H2: scalar space degree > 4 not instantiated");
+      }
+    } else if (kind == kHelmholtz) {
+      switch (q) {
+        case 0: assemble_impl<HelmT<0>>(); break;
+        case 1: assemble_impl<HelmT<1>>(); break;
+        case 2: assemble_impl<HelmT<2>>(); break;
+        case 3: assemble_impl<HelmT<3>>(); break;
+        case 4: assemble_impl<HelmT<4>>(); break;
+        default: throw std::invalid_argument("B200 H2: scalar space degree > 4 not instantiated");
+      }
+    } else {
+      switch (q) {
+        case 1: assemble_impl<MaxT<1>>(); break;
+        case 2: assemble_impl<MaxT<2>>(); break;
+        case 3: assemble_impl<MaxT<3>>(); break;
+        default: throw std::invalid_argument("B200 H2: Maxwell degree > 3 not instantiated");
+      }
+    }
+  } catch (...) {
+    for (void* p : allocs_) cudaFree(p);
+    allocs_.clear();
+    if (stream_) cudaStreamDestroy(stream_);
+    stream_ = nullptr;
+    throw;
+  }
+  times_.total_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall0).count();
+}
+
+H2Device::~H2Device() {
+  cudaSetDevice(device_);
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  for (void* p : allocs_) cudaFree(p);
+  if (h_x_pinned_) cudaFreeHost(h_x_pinned_);
+  if (h_y_pinned_) cudaFreeHost(h_y_pinned_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+template <class KT>
+void H2Device::assemble_impl() {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL, NC = KT::NC;
+  const Discretization& d = *disc_;
+  const H2Plan& P = plan_;
+  if (d.local_count() != NL) throw std::logic_error("B200 H2: local count mismatch");
+  const int ne = d.element_count(), m = P.m, mm = m * m, rows = nch_ * mm;
+  const int sw = sizeof(S) / 8;
+  const cplx kap = d.kappa();
+  KParams kp;
+  kp.kr = kap.real();
+  kp.ki = kap.imag();
+  if (d.is_vector()) {
+    const cplx dw = -1.0 / (kap * kap);
+    kp.dwx = dw.real();
+    kp.dwy = dw.imag();
+  } else {
+    kp.dwx = kp.dwy = 0.0;
+  }
+  cudaEvent_t ev[10];
+  for (auto& e : ev) IGB_CUDA(cudaEventCreate(&e));
+  IGB_CUDA(cudaEventRecord(ev[0], stream_));
+
+  // ---- upload
+  std::vector<double> cells(d.cells().size() * kCellStride, 0.0);
+  for (size_t c = 0; c < d.cells().size(); ++c) {
+    const GeomCell& gc = d.cells()[c];
+    for (int comp = 0; comp < 4; ++comp)
+      for (int j = 0; j <= kMaxGeomDeg; ++j)
+        for (int i = 0; i <= kMaxGeomDeg; ++i) cells[c * kCellStride + comp * 25 + j * 5 + i] = gc.coef[comp][j][i];
+    cells[c * kCellStride + 100] = gc.u0;
+    cells[c * kCellStride + 101] = gc.v0;
+  }
+  d_cells_ = upload(cells);
+  d_el_cell_ = upload(d.element_cell());
+  {
+    std::vector<int> info;
+    std::vector<double> knots;
+    int base = 0;
+    for (int p = 0; p < d.geometry().patch_count(); ++p) {
+      const Patch& s = d.geometry().patch(p);
+      const int ku_off = static_cast<int>(knots.size());
+      knots.insert(knots.end(), s.kv_u.knots.begin(), s.kv_u.knots.end());
+      const int kv_off = static_cast<int>(knots.size());
+      knots.insert(knots.end(), s.kv_v.knots.begin(), s.kv_v.knots.end());
+      info.insert(info.end(), {base, s.kv_u.degree, s.kv_v.degree, static_cast<int>(s.kv_u.knots.size()),
+                               static_cast<int>(s.kv_v.knots.size()), ku_off, kv_off});
+      base += (s.kv_u.size() - s.kv_u.degree) * (s.kv_v.size() - s.kv_v.degree);
+    }
+    d_patch_info_ = upload(info);
+    d_knots_ = upload(knots);
+  }
+  d_tab_a_ = upload(d.is_vector() ? d.tab_p() : d.tab_s());
+  d_tab_b_ = upload(d.is_vector() ? d.tab_q() : std::vector<double>(1, 0.0));
+  d_l2g_ = upload(d.l2g());
+  d_lsign_ = upload(d.lsign());
+  d_near_a_ = upload(P.near_a);
+  d_near_b_ = upload(P.near_b);
+  d_near_rs_ = upload(P.near_row_start);
+  d_far_a_ = upload(P.far_a);
+  d_far_b_ = upload(P.far_b);
+  d_far_rs_ = upload(P.far_row_start);
+  {
+    std::vector<int> targets;
+    for (int t = 0; t < P.n_nodes; ++t)
+      if (P.far_row_start[t + 1] > P.far_row_start[t]) targets.push_back(t);
+    n_far_targets_ = static_cast<int>(targets.size());
+    d_far_targets_ = upload(targets);
+  }
+  d_dof_start_ = upload(P.dof_start);
+  d_dof_inc_ = upload(P.dof_inc);
+  d_tl_ = upload(P.tl);
+  d_tr_ = upload(P.tr);
+  int* d_np = upload(P.node_patch);
+  int* d_nl = upload(P.node_level);
+  int* d_nsx = upload(P.node_sx);
+  int* d_nsy = upload(P.node_sy);
+  double* d_cheb = upload(P.cheb);
+  std::vector<double> gxf, gwf, gxs, gws;
+  gauss_rule(P.nfar, gxf, gwf);
+  gauss_rule(P.nsing, gxs, gws);
+  double* d_gxf = upload(gxf);
+  double* d_gwf = upload(gwf);
+  double* d_gxs = upload(gxs);
+  double* d_gws = upload(gws);
+  std::vector<double> lag(static_cast<size_t>(m) * P.nfar);
+  {
+    std::vector<double> tmp(m);
+    for (int a = 0; a < P.nfar; ++a) {
+      lagrange_all(P.cheb, gxf[a], tmp.data());
+      for (int i = 0; i < m; ++i) lag[i * P.nfar + a] = tmp[i];
+    }
+  }
+  double* d_lag = upload(lag);
+  std::vector<int> sing_d[4][4];
+  std::vector<unsigned char> sing_m[4][2];
+  int* d_sing[4][4] = {};
+  unsigned char* d_singm[4][2] = {};
+  for (int c = 1; c <= 3; ++c) {
+    const auto& L = P.sing[c];
+    d_sing[c][0] = upload(L.ea);
+    d_sing[c][1] = upload(L.eb);
+    d_sing[c][2] = upload(L.slot_ab);
+    d_sing[c][3] = upload(L.slot_ba);
+    d_singm[c][0] = upload(L.map_a);
+    d_singm[c][1] = upload(L.map_b);
+  }
+  int* d_reg = upload(P.reg_slot);
+
+  const long long nnear = static_cast<long long>(P.near_a.size());
+  const long long nfarp = static_cast<long long>(P.far_a.size());
+  const int nf = P.nfar, nq = nf * nf;
+  d_near_ = dalloc<double>(static_cast<size_t>(nnear) * NL * NL * sw);
+  d_far_ = dalloc<double>(static_cast<size_t>(nfarp) * mm * mm * sw);
+  d_mom_ = dalloc<double>(static_cast<size_t>(ne) * NL * rows);
+  d_img_ = dalloc<double>(static_cast<size_t>(P.n_nodes) * mm * 3);
+  d_cpts_ = dalloc<double>(static_cast<size_t>(ne) * nq * 3);
+  d_cval_ = dalloc<double>(static_cast<size_t>(ne) * NC * nq * NL);
+  bytes_.near = static_cast<size_t>(nnear) * NL * NL * 8 * sw;
+  bytes_.far = static_cast<size_t>(nfarp) * mm * mm * 8 * sw;
+  bytes_.moments = static_cast<size_t>(ne) * NL * rows * 8;
+  IGB_CUDA(cudaEventRecord(ev[1], stream_));
+
+  GeoArgs g;
+  g.cells = d_cells_;
+  g.el_cell = d_el_cell_;
+  g.tab_a = d_tab_a_;
+  g.tab_b = d_tab_b_;
+  g.level = d.level();
+  g.epp = d.elements_per_patch();
+  g.h = 1.0 / (1 << d.level());
+  g.kp = kp;
+
+  // ---- K1 element caches + moments
+  {
+    const size_t smem = (104 + KT::TABN + static_cast<size_t>(nq) * NC * NL) * 8;
+    IGB_CUDA(cudaFuncSetAttribute(k_element<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (ne > 0) k_element<KT><<<ne, 128, smem, stream_>>>(g, nf, d_gxf, d_gwf, m, d_lag, d_cpts_, d_cval_, d_mom_);
+    IGB_CUDA(cudaGetLastError());
+  }
+  IGB_CUDA(cudaEventRecord(ev[2], stream_));
+  // ---- K2 images
+  {
+    const long long tot = static_cast<long long>(P.n_nodes) * mm;
+    PatchDev pd{d_patch_info_, d_knots_};
+    k_images<<<grid_for(tot, 256), 256, 0, stream_>>>(P.n_nodes, m, d_cheb, d_np, d_nl, d_nsx, d_nsy, pd, d_cells_,
+                                                       d_img_);
+    IGB_CUDA(cudaGetLastError());
+  }
+  IGB_CUDA(cudaEventRecord(ev[3], stream_));
+  // ---- K3 couplings
+  if (nfarp > 0) {
+    k_couplings<KT><<<148 * 16, 256, 0, stream_>>>(nfarp, mm, d_far_a_, d_far_b_, d_img_, kp, d_far_);
+    IGB_CUDA(cudaGetLastError());
+  }
+  IGB_CUDA(cudaEventRecord(ev[4], stream_));
+  // ---- K4 regular near
+  if (!P.reg_slot.empty()) {
+    const size_t smem = static_cast<size_t>(NC) * nq * NL * 8 * sw;
+    IGB_CUDA(cudaFuncSetAttribute(k_regular<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (smem > 200 * 1024) throw std::invalid_argument("B200 H2: far quadrature order too large");
+    k_regular<KT><<<static_cast<unsigned>(P.reg_slot.size()), 128, smem, stream_>>>(
+        d_reg, d_near_a_, d_near_b_, d_near_rs_, nq, d_cpts_, d_cval_, kp, d_near_);
+    IGB_CUDA(cudaGetLastError());
+  }
+  IGB_CUDA(cudaEventRecord(ev[5], stream_));
+  // ---- K5 singular near, batched by class
+  {
+    using LY = SingLayout<KT>;
+    if (P.nsing > 64) throw std::invalid_argument("gauss_rule: order out of range");
+    if (P.nsing > 16) throw std::invalid_argument("B200 H2: singular order > 16 not supported (32-bit point index)");
+    auto launch = [&](auto cls_tag, int c, int evi) {
+      constexpr int CLS = decltype(cls_tag)::value;
+      const auto& L = P.sing[c];
+      if (!L.ea.empty()) {
+        SingArgs A;
+        A.n_pairs = static_cast<int>(L.ea.size());
+        A.n = P.nsing;
+        A.ea = d_sing[c][0];
+        A.eb = d_sing[c][1];
+        A.slot_ab = d_sing[c][2];
+        A.slot_ba = d_sing[c][3];
+        A.map_a = d_singm[c][0];
+        A.map_b = d_singm[c][1];
+        A.gx = d_gxs;
+        A.gw = d_gws;
+        A.near_a = d_near_a_;
+        A.near_rs = d_near_rs_;
+        A.near = d_near_;
+        IGB_CUDA(cudaFuncSetAttribute(k_singular<KT, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(LY::BYTES)));
+        k_singular<KT, CLS><<<A.n_pairs, 128, LY::BYTES, stream_>>>(g, A);
+        IGB_CUDA(cudaGetLastError());
+      }
+      IGB_CUDA(cudaEventRecord(ev[evi], stream_));
+    };
+    launch(std::integral_constant<int, 3>{}, 3, 6);
+    launch(std::integral_constant<int, 2>{}, 2, 7);
+    launch(std::integral_constant<int, 1>{}, 1, 8);
+  }
+  // ---- matvec scratch
+  const size_t nn = static_cast<size_t>(P.n_nodes);
+  dx_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
+  dy_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
+  d_coef_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
+  d_up_ = dalloc<double>(nn * rows * sw);
+  d_down_ = dalloc<double>(nn * rows * sw);
+  d_loc_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
+  IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
+  IGB_CUDA(cudaEventRecord(ev[9], stream_));
+  IGB_CUDA(cudaStreamSynchronize(stream_));
+  float ms = 0;
+  auto el = [&](int a, int b) {
+    IGB_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+    return static_cast<double>(ms);
+  };
+  times_.upload = el(0, 1);
+  times_.elements = el(1, 2);
+  times_.images = el(2, 3);
+  times_.couplings = el(3, 4);
+  times_.regular = el(4, 5);
+  times_.singular[3] = el(5, 6);
+  times_.singular[2] = el(6, 7);
+  times_.singular[1] = el(7, 8);
+  times_.total_device = el(1, 8);
+  for (auto& e : ev) cudaEventDestroy(e);
+  bytes_.other = 0;
+}
+
+template <class KT>
+void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL;
+  const Discretization& d = *disc_;
+  const H2Plan& P = plan_;
+  const int ne = d.element_count(), m = P.m, mm = m * m, rows = nch_ * mm, L = P.depth;
+  const int np = P.n_patches, npp = P.npp, epp = d.elements_per_patch();
+  const S* x = reinterpret_cast<const S*>(xin);
+  S* y = reinterpret_cast<S*>(yout);
+  S* coef = reinterpret_cast<S*>(d_coef_);
+  S* up = reinterpret_cast<S*>(d_up_);
+  S* down = reinterpret_cast<S*>(d_down_);
+  S* loc = reinterpret_cast<S*>(d_loc_);
+  int launches = 0;
+  const int nloc = ne * NL;
+  k_coef<S><<<grid_for(nloc, 256), 256, 0, s>>>(nloc, x, d_l2g_, d_lsign_, coef);
+  ++launches;
+  k_leaf_up<S><<<grid_for(static_cast<long long>(ne) * rows, 256), 256, 0, s>>>(ne, NL, rows, epp, npp,
+                                                                                 P.level_offset[L], d_mom_, coef, up);
+  ++launches;
+  for (int l = L - 1; l >= 0; --l) {
+    const long long tot = static_cast<long long>(np) * (1LL << (2 * l)) * rows;
+    k_up_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                                                      d_tl_, d_tr_, up);
+    ++launches;
+  }
+  const size_t ndown = static_cast<size_t>(P.n_nodes) * rows;
+  k_zero<S><<<grid_for(static_cast<long long>(ndown), 256), 256, 0, s>>>(ndown, down);
+  ++launches;
+  if (n_far_targets_ > 0) {
+    S dw;
+    if constexpr (sizeof(S) == 8) {
+      dw = 1.0;
+    } else {
+      const cplx kap = d.kappa();
+      const cplx w = d.is_vector() ? -1.0 / (kap * kap) : cplx(1.0, 0.0);
+      dw = mk(w.real(), w.imag());
+    }
+    const unsigned grid = grid_for(static_cast<long long>(n_far_targets_) * 32, 256);
+    const S* K = reinterpret_cast<const S*>(d_far_);
+    if (nch_ == 4) {
+      if (mm <= 32) k_far<S, 4, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+      else if (mm <= 64) k_far<S, 4, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+      else k_far<S, 4, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+    } else {
+      if (mm <= 32) k_far<S, 1, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+      else if (mm <= 64) k_far<S, 1, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+      else k_far<S, 1, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+    }
+    ++launches;
+  }
+  for (int l = 0; l < L; ++l) {
+    const long long tot = static_cast<long long>(np) * (4LL << (2 * l)) * rows;
+    k_down_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, l, npp, P.level_offset[l], P.level_offset[l + 1], m,
+                                                        nch_, d_tl_, d_tr_, down);
+    ++launches;
+  }
+  k_near_leaf<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, s>>>(
+      ne, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, rows, epp, npp, P.level_offset[L], d_mom_,
+      down, loc);
+  ++launches;
+  k_scatter<S><<<grid_for(d.dof_count(), 256), 256, 0, s>>>(d.dof_count(), d_dof_start_, d_dof_inc_, d_lsign_, loc, y);
+  ++launches;
+  IGB_CUDA(cudaGetLastError());
+  apply_launches_ = launches;
+}
+
+void H2Device::enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s) {
+  const int kind = disc_->kind();
+  const int q = kind == kMaxwell ? disc_->degree() : disc_->scalar_degree();
+  if (kind == kLaplace) {
+    switch (q) {
+      case 0: enqueue_apply<LapT<0>>(x, y, s); break;
+      case 1: enqueue_apply<LapT<1>>(x, y, s); break;
+      case 2: enqueue_apply<LapT<2>>(x, y, s); break;
+      case 3: enqueue_apply<LapT<3>>(x, y, s); break;
+      default: enqueue_apply<LapT<4>>(x, y, s); break;
+    }
+  } else if (kind == kHelmholtz) {
+    switch (q) {
+      case 0: enqueue_apply<HelmT<0>>(x, y, s); break;
+      case 1: enqueue_apply<HelmT<1>>(x, y, s); break;
+      case 2: enqueue_apply<HelmT<2>>(x, y, s); break;
+      case 3: enqueue_apply<HelmT<3>>(x, y, s); break;
+      default: enqueue_apply<HelmT<4>>(x, y, s); break;
+    }
+  } else {
+    switch (q) {
+      case 1: enqueue_apply<MaxT<1>>(x, y, s); break;
+      case 2: enqueue_apply<MaxT<2>>(x, y, s); break;
+      default: enqueue_apply<MaxT<3>>(x, y, s); break;
+    }
+  }
+}
+
+void H2Device::launch_apply_graph(cudaStream_t s) {
+  IGB_CUDA(cudaSetDevice(device_));
+  if (!graph_exec_) {
+    cudaGraph_t graph;
+    IGB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue_apply_dispatch(dx_, dy_, stream_);
+    IGB_CUDA(cudaStreamEndCapture(stream_, &graph));
+    IGB_CUDA(cudaGraphInstantiate(&graph_exec_, graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  IGB_CUDA(cudaGraphLaunch(graph_exec_, s));
+}
+
+void H2Device::apply_device(const double* x, double* y, cudaStream_t s) {
+  const size_t bytes = static_cast<size_t>(dim()) * (is_complex() ? 16 : 8);
+  IGB_CUDA(cudaSetDevice(device_));
+  if (s == nullptr) s = stream_;
+  IGB_CUDA(cudaMemcpyAsync(dx_, x, bytes, cudaMemcpyDeviceToDevice, s));
+  launch_apply_graph(s);
+  IGB_CUDA(cudaMemcpyAsync(y, dy_, bytes, cudaMemcpyDeviceToDevice, s));
+}
+
+void H2Device::apply_host(const double* x, double* y) {
+  const size_t bytes = static_cast<size_t>(dim()) * (is_complex() ? 16 : 8);
+  IGB_CUDA(cudaSetDevice(device_));
+  if (!h_x_pinned_) {
+    IGB_CUDA(cudaMallocHost(&h_x_pinned_, bytes));
+    IGB_CUDA(cudaMallocHost(&h_y_pinned_, bytes));
+  }
+  std::memcpy(h_x_pinned_, x, bytes);
+  IGB_CUDA(cudaMemcpyAsync(dx_, h_x_pinned_, bytes, cudaMemcpyHostToDevice, stream_));
+  launch_apply_graph(stream_);
+  IGB_CUDA(cudaMemcpyAsync(h_y_pinned_, dy_, bytes, cudaMemcpyDeviceToHost, stream_));
+  IGB_CUDA(cudaStreamSynchronize(stream_));
+  std::memcpy(y, h_y_pinned_, bytes);
+}
+
+void H2Device::near_blocks(long long first, long long count, double* out) const {
+  const int nl = disc_->local_count(), sw = is_complex() ? 2 : 1;
+  if (first < 0 || first + count > static_cast<long long>(plan_.near_a.size()))
+    throw std::invalid_argument("near_blocks: range out of bounds");
+  IGB_CUDA(cudaSetDevice(device_));
+  if (count == 0) return;
+  // rows touched by the range
+  const int e0 = plan_.near_a[first], e1 = plan_.near_a[first + count - 1];
+  const int r0 = plan_.near_row_start[e0], r1 = plan_.near_row_start[e1 + 1];
+  std::vector<double> buf(static_cast<size_t>(r1 - r0) * nl * nl * sw);
+  IGB_CUDA(cudaMemcpy(buf.data(), d_near_ + static_cast<size_t>(r0) * nl * nl * sw, buf.size() * 8,
+                      cudaMemcpyDeviceToHost));
+  for (long long q = first; q < first + count; ++q) {
+    const int e = plan_.near_a[q], rs = plan_.near_row_start[e], cnt = plan_.near_row_start[e + 1] - rs;
+    for (int la = 0; la < nl; ++la)
+      for (int lb = 0; lb < nl; ++lb) {
+        const size_t src = static_cast<size_t>(rs - r0) * nl * nl + (static_cast<size_t>(la) * cnt + (q - rs)) * nl + lb;
+        const size_t dst = (static_cast<size_t>(q - first) * nl + la) * nl + lb;
+        for (int c = 0; c < sw; ++c) out[dst * sw + c] = buf[src * sw + c];
+      }
+  }
+}
+void H2Device::couplings(long long first, long long count, double* out) const {
+  const size_t per = static_cast<size_t>(plan_.m) * plan_.m * plan_.m * plan_.m * (is_complex() ? 2 : 1);
+  if (first < 0 || first + count > static_cast<long long>(plan_.far_a.size()))
+    throw std::invalid_argument("couplings: range out of bounds");
+  IGB_CUDA(cudaSetDevice(device_));
+  IGB_CUDA(cudaMemcpy(out, d_far_ + first * per, count * per * 8, cudaMemcpyDeviceToHost));
+}
+void H2Device::moments(double* out) const {
+  IGB_CUDA(cudaSetDevice(device_));
+  IGB_CUDA(cudaMemcpy(out, d_mom_, bytes_.moments, cudaMemcpyDeviceToHost));
+}
+void H2Device::images(double* out) const {
+  IGB_CUDA(cudaSetDevice(device_));
+  IGB_CUDA(cudaMemcpy(out, d_img_, static_cast<size_t>(plan_.n_nodes) * plan_.m * plan_.m * 3 * 8,
+                      cudaMemcpyDeviceToHost));
+}
+
+}  // namespace igb

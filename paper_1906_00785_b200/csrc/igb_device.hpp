@@ -1,0 +1,106 @@
+// Device-resident H² operator (assembly + matvec on one B200).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "igb_host.hpp"
+
+namespace igb {
+
+struct AssemblyTimes {  // milliseconds, CUDA events on the assembly stream
+  double plan_host = 0, upload = 0, elements = 0, images = 0, couplings = 0, regular = 0,
+         singular[4] = {0, 0, 0, 0}, total_device = 0, total_wall = 0;
+};
+
+struct DeviceBytes {
+  size_t near = 0, far = 0, moments = 0, other = 0;
+};
+
+class H2Device {
+ public:
+  // flags bit0: keep the element quadrature caches resident (introspection)
+  H2Device(std::shared_ptr<const Discretization> d, int m, double eta, int far_order,
+           int sing_order, int device, int flags = 0);
+  ~H2Device();
+  H2Device(const H2Device&) = delete;
+  H2Device& operator=(const H2Device&) = delete;
+
+  const Discretization& disc() const { return *disc_; }
+  const H2Plan& plan() const { return plan_; }
+  bool is_complex() const { return disc_->is_complex(); }
+  int dim() const { return disc_->dof_count(); }
+  int nch() const { return nch_; }
+  int m() const { return plan_.m; }
+  int device() const { return device_; }
+  cudaStream_t stream() const { return stream_; }
+  const AssemblyTimes& times() const { return times_; }
+  DeviceBytes bytes() const { return bytes_; }
+
+  // y = H x.  Scalars are double or interleaved complex<double>.
+  void apply_host(const double* x, double* y);
+  void apply_device(const double* x, double* y, cudaStream_t s);
+  // launches of the matvec graph without copies (benchmarking): x/y are the
+  // internal buffers
+  double* x_buffer() { return dx_; }
+  double* y_buffer() { return dy_; }
+  void launch_apply_graph(cudaStream_t s);
+  int apply_kernel_launches() const { return apply_launches_; }
+
+  // introspection (host copies, reference layouts)
+  void near_blocks(long long first, long long count, double* out) const;  // [q][la][lb]
+  void couplings(long long first, long long count, double* out) const;    // [q][mu][nu] (col-major K)
+  void moments(double* out) const;                                        // [e][l][row] real
+  void images(double* out) const;                                         // [node][nu][3]
+
+ private:
+  template <class KT> void assemble_impl();
+  template <class KT> void enqueue_apply(const double* x, double* y, cudaStream_t s);
+  void enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s);
+
+  std::shared_ptr<const Discretization> disc_;
+  H2Plan plan_;
+  int device_ = 0, nch_ = 1, flags_ = 0;
+  cudaStream_t stream_ = nullptr;
+  AssemblyTimes times_;
+  DeviceBytes bytes_;
+
+  // device arrays (raw allocations, owned)
+  std::vector<void*> allocs_;
+  template <class T> T* dalloc(size_t n);
+  template <class T> T* upload(const std::vector<T>& v);
+
+  // geometry / space
+  double* d_cells_ = nullptr;       // [cell][100] coefficients + [cell][2] origins
+  int* d_el_cell_ = nullptr;        // [e]
+  int* d_patch_info_ = nullptr;     // per patch: cell_base, pu, pv, nku, nkv, ku_off, kv_off
+  double* d_knots_ = nullptr;
+  double* d_tab_a_ = nullptr;       // scalar: tab_s; Maxwell: tab_p
+  double* d_tab_b_ = nullptr;       // Maxwell: tab_q
+  int* d_l2g_ = nullptr;
+  double* d_lsign_ = nullptr;
+  // plan
+  int *d_near_a_ = nullptr, *d_near_b_ = nullptr, *d_near_rs_ = nullptr;
+  int *d_far_b_ = nullptr, *d_far_rs_ = nullptr, *d_far_targets_ = nullptr;
+  int n_far_targets_ = 0;
+  int *d_far_a_ = nullptr;
+  int *d_dof_start_ = nullptr, *d_dof_inc_ = nullptr;
+  double *d_tl_ = nullptr, *d_tr_ = nullptr;
+  // operator data
+  double* d_near_ = nullptr;   // row layout [e][la][k][lb], Scalar
+  double* d_far_ = nullptr;    // [q][mu][nu], Scalar
+  double* d_mom_ = nullptr;    // [e][l][row], real
+  double* d_img_ = nullptr;    // [node][nu][3]
+  double* d_cpts_ = nullptr;   // element caches (assembly scratch)
+  double* d_cval_ = nullptr;
+  // matvec scratch (Scalar)
+  double *dx_ = nullptr, *dy_ = nullptr, *d_coef_ = nullptr, *d_up_ = nullptr, *d_down_ = nullptr,
+         *d_loc_ = nullptr;
+  double *h_x_pinned_ = nullptr, *h_y_pinned_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int apply_launches_ = 0;
+};
+
+}  // namespace igb

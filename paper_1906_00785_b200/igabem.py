@@ -1,0 +1,435 @@
+"""Python mirror of the reference's C++ API for the H² hot path, over the C ABI.
+
+Names, argument meaning and error behaviour follow igabem
+(/root/reference/proj/core/include/igabem): ``make_sphere`` / ``make_square``
+(shapes.hpp), ``Pde`` (pde.hpp), ``Discretization`` (spaces.hpp),
+``H2Options`` / ``AssemblyOptions`` (h2.hpp, assembly.hpp) and
+``H2Matrix`` (h2.hpp:57-106).  Exceptions map the reference's C++ exception
+types: std::invalid_argument -> ValueError, std::logic_error ->
+LogicError, std::runtime_error -> RuntimeError, std::domain_error ->
+DomainError.  There is no CPU fallback: every operator call runs the CUDA
+kernels of libigabem_b200.so, and a missing library or device raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libigabem_b200.so")
+_LIB = None
+
+
+class LogicError(RuntimeError):
+    """std::logic_error"""
+
+
+class DomainError(ValueError):
+    """std::domain_error"""
+
+
+class CudaError(RuntimeError):
+    """device failure"""
+
+
+_EXC = {1: ValueError, 2: LogicError, 3: RuntimeError, 4: DomainError, 5: CudaError}
+
+LAPLACE, HELMHOLTZ, MAXWELL = 0, 1, 2
+FAR, VERTEX, EDGE, COINCIDENT = 0, 1, 2, 3
+
+
+class _DiscInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("dof_count", "element_count", "local_count", "level", "degree",
+                                            "repetition", "kind", "patch_count")]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int), ("eta", ctypes.c_double), ("far_order", ctypes.c_int),
+                ("sing_order", ctypes.c_int)]
+
+
+class _Storage(ctypes.Structure):
+    _fields_ = [("nearfield_entries", ctypes.c_size_t), ("farfield_entries", ctypes.c_size_t),
+                ("total_bytes", ctypes.c_size_t)]
+
+
+class _Times(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("plan_host_ms", "upload_ms", "elements_ms", "images_ms",
+                                               "couplings_ms", "regular_ms", "coincident_ms", "edge_ms",
+                                               "vertex_ms", "device_total_ms", "wall_total_ms")]
+
+
+class _PatchDesc(ctypes.Structure):
+    _fields_ = [("degree_u", ctypes.c_int), ("degree_v", ctypes.c_int), ("n_knots_u", ctypes.c_int),
+                ("n_knots_v", ctypes.c_int), ("knots_u", ctypes.POINTER(ctypes.c_double)),
+                ("knots_v", ctypes.POINTER(ctypes.c_double)), ("ctrl_w", ctypes.POINTER(ctypes.c_double)),
+                ("weight", ctypes.POINTER(ctypes.c_double))]
+
+
+SYMBOLS = (
+    "igb_geometry_create", "igb_geometry_sphere", "igb_geometry_square", "igb_geometry_info",
+    "igb_geometry_destroy", "igb_discretization_create", "igb_discretization_info", "igb_discretization_l2g",
+    "igb_discretization_elements", "igb_classify_pair", "igb_discretization_destroy", "igb_h2_create",
+    "igb_h2_dim", "igb_h2_apply", "igb_h2_apply_device", "igb_h2_storage_report", "igb_h2_counts",
+    "igb_h2_near_pairs", "igb_h2_far_pairs", "igb_h2_tree", "igb_h2_near_blocks", "igb_h2_couplings",
+    "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
+    "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
+)
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libigabem_b200.so (built in-tree by __graft_entry__.build())."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(_LIB_PATH)
+    vp, i32, f64, i64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong, ctypes.c_size_t
+    P = ctypes.POINTER
+    L.igb_geometry_create.argtypes = [i32, P(_PatchDesc), P(vp)]
+    L.igb_geometry_sphere.argtypes = [f64, P(f64), P(vp)]
+    L.igb_geometry_square.argtypes = [P(vp)]
+    L.igb_geometry_info.argtypes = [vp, P(i32), P(i32), P(i32)]
+    L.igb_geometry_destroy.argtypes = [vp]
+    L.igb_geometry_destroy.restype = None
+    L.igb_discretization_create.argtypes = [vp, i32, f64, f64, i32, i32, i32, P(vp)]
+    L.igb_discretization_info.argtypes = [vp, P(_DiscInfo)]
+    L.igb_discretization_l2g.argtypes = [vp, P(i32), P(f64)]
+    L.igb_discretization_elements.argtypes = [vp, P(i32), P(f64)]
+    L.igb_classify_pair.argtypes = [vp, i32, i32, P(i32), P(i32)]
+    L.igb_discretization_destroy.argtypes = [vp]
+    L.igb_discretization_destroy.restype = None
+    L.igb_h2_create.argtypes = [vp, P(_Opts), i32, P(vp)]
+    L.igb_h2_dim.argtypes = [vp, P(i32)]
+    L.igb_h2_apply.argtypes = [vp, P(f64), P(f64)]
+    L.igb_h2_apply_device.argtypes = [vp, vp, vp, vp]
+    L.igb_h2_storage_report.argtypes = [vp, P(_Storage)]
+    L.igb_h2_counts.argtypes = [vp, P(i64), P(i64), P(i32)]
+    L.igb_h2_near_pairs.argtypes = [vp, P(i32)]
+    L.igb_h2_far_pairs.argtypes = [vp, P(i32)]
+    L.igb_h2_tree.argtypes = [vp, P(i32), P(i32), P(i32), P(i32), P(f64)]
+    L.igb_h2_near_blocks.argtypes = [vp, i64, i64, P(f64)]
+    L.igb_h2_couplings.argtypes = [vp, i64, i64, P(f64)]
+    L.igb_h2_moments.argtypes = [vp, P(f64)]
+    L.igb_h2_images.argtypes = [vp, P(f64)]
+    L.igb_h2_assembly_times.argtypes = [vp, P(_Times)]
+    L.igb_h2_device_bytes.argtypes = [vp, P(sz), P(sz), P(sz)]
+    L.igb_h2_bench_apply.argtypes = [vp, i32, P(ctypes.c_float), P(i32)]
+    L.igb_h2_destroy.argtypes = [vp]
+    L.igb_h2_destroy.restype = None
+    L.igb_admissible.argtypes = [P(f64), P(f64), f64]
+    L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
+    _LIB = L
+    return L
+
+
+def _p(a, t=ctypes.c_double):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def _check(rc):
+    if rc != 0:
+        buf = ctypes.create_string_buffer(1024)
+        lib().igb_last_error(buf, 1024)
+        raise _EXC.get(rc, RuntimeError)(buf.value.decode())
+
+
+# ------------------------------------------------------------------ pde.hpp
+@dataclass(frozen=True)
+class Pde:
+    """Pde{kind, kappa} (pde.hpp:9-27)."""
+    kind: int = LAPLACE
+    kappa: complex = 0j
+
+    def is_complex(self):
+        return self.kind != LAPLACE
+
+    def is_vector(self):
+        return self.kind == MAXWELL
+
+    @staticmethod
+    def laplace():
+        return Pde(LAPLACE, 0j)
+
+    @staticmethod
+    def helmholtz(k):
+        return Pde(HELMHOLTZ, complex(k))
+
+    @staticmethod
+    def maxwell(k):
+        if complex(k) == 0:
+            raise ValueError("Pde: Maxwell requires a nonzero wavenumber")
+        return Pde(MAXWELL, complex(k))
+
+
+# ------------------------------------------------------------- geometry.hpp
+class Geometry:
+    """Multi-patch NURBS geometry (geometry.hpp:38-76)."""
+
+    def __init__(self, patches=None, _handle=None):
+        if _handle is None:
+            descs = (_PatchDesc * len(patches))()
+            keep = []
+            for i, p in enumerate(patches):
+                ku = np.ascontiguousarray(p["knots_u"], dtype=np.float64)
+                kv = np.ascontiguousarray(p["knots_v"], dtype=np.float64)
+                cw = np.ascontiguousarray(p["ctrl_w"], dtype=np.float64)
+                w = np.ascontiguousarray(p["weight"], dtype=np.float64)
+                keep += [ku, kv, cw, w]
+                descs[i] = _PatchDesc(p["degree_u"], p["degree_v"], len(ku), len(kv), _p(ku), _p(kv), _p(cw), _p(w))
+            h = ctypes.c_void_p()
+            _check(lib().igb_geometry_create(len(patches), descs, ctypes.byref(h)))
+            _handle = h
+        self._h = _handle
+        n = [ctypes.c_int() for _ in range(3)]
+        _check(lib().igb_geometry_info(self._h, *[ctypes.byref(x) for x in n]))
+        self._np, self._ne, self._nv = (x.value for x in n)
+
+    def patch_count(self):
+        return self._np
+
+    def edge_count(self):
+        return self._ne
+
+    def vertex_count(self):
+        return self._nv
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.igb_geometry_destroy(self._h)
+            self._h = None
+
+
+def make_sphere(radius=1.0, center=(0.0, 0.0, 0.0)) -> Geometry:
+    """Exact six-patch rational sphere (shapes.hpp:21-22, shapes.cpp:87-205)."""
+    c = np.asarray(center, dtype=np.float64)
+    h = ctypes.c_void_p()
+    _check(lib().igb_geometry_sphere(float(radius), _p(c), ctypes.byref(h)))
+    return Geometry(_handle=h)
+
+
+def make_square() -> Geometry:
+    """Unit square in z = 0 (shapes.hpp:16, shapes.cpp:28-30)."""
+    h = ctypes.c_void_p()
+    _check(lib().igb_geometry_square(ctypes.byref(h)))
+    return Geometry(_handle=h)
+
+
+# --------------------------------------------------------------- spaces.hpp
+class Discretization:
+    """Discrete ansatz space (spaces.hpp:37-105): Discretization(g, pde, degree, rep, level)."""
+
+    def __init__(self, geometry: Geometry, pde: Pde, degree: int, rep: int, level: int):
+        h = ctypes.c_void_p()
+        _check(lib().igb_discretization_create(geometry._h, pde.kind, pde.kappa.real, pde.kappa.imag, int(degree),
+                                               int(rep), int(level), ctypes.byref(h)))
+        self._h = h
+        self._geometry = geometry
+        self._pde = pde
+        info = _DiscInfo()
+        _check(lib().igb_discretization_info(h, ctypes.byref(info)))
+        self._info = info
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.igb_discretization_destroy(self._h)
+            self._h = None
+
+    def geometry(self):
+        return self._geometry
+
+    def pde(self):
+        return self._pde
+
+    def degree(self):
+        return self._info.degree
+
+    def repetition(self):
+        return self._info.repetition
+
+    def level(self):
+        return self._info.level
+
+    def dof_count(self):
+        return self._info.dof_count
+
+    def element_count(self):
+        return self._info.element_count
+
+    def local_count(self):
+        return self._info.local_count
+
+    def elements_per_patch(self):
+        return 1 << (2 * self._info.level)
+
+    def element_index(self, patch, ix, iy):
+        return patch * self.elements_per_patch() + ix + (1 << self._info.level) * iy
+
+    def local_to_global(self):
+        n = self.element_count() * self.local_count()
+        g = np.zeros(n, dtype=np.int32)
+        s = np.zeros(n)
+        _check(lib().igb_discretization_l2g(self._h, _p(g, ctypes.c_int), _p(s)))
+        return g.reshape(self.element_count(), -1), s.reshape(self.element_count(), -1)
+
+    def elements(self):
+        ints = np.zeros((self.element_count(), 3), dtype=np.int32)
+        dbl = np.zeros((self.element_count(), 9))
+        _check(lib().igb_discretization_elements(self._h, _p(ints, ctypes.c_int), _p(dbl)))
+        return ints, dbl
+
+    def classify_pair(self, ea, eb):
+        cls = ctypes.c_int()
+        maps = np.zeros(6, dtype=np.int32)
+        _check(lib().igb_classify_pair(self._h, int(ea), int(eb), ctypes.byref(cls), _p(maps, ctypes.c_int)))
+        return cls.value, maps
+
+
+# ------------------------------------------------------------------- h2.hpp
+@dataclass
+class AssemblyOptions:
+    """AssemblyOptions (assembly.hpp:13-20); 0 -> P+2 (far) / P+3 (singular)."""
+    far_order: int = 0
+    sing_order: int = 0
+
+
+@dataclass
+class H2Options:
+    """H2Options{m = 8, eta = 1.6, quad} (h2.hpp:11-15)."""
+    m: int = 8
+    eta: float = 1.6
+    quad: AssemblyOptions = field(default_factory=AssemblyOptions)
+
+
+@dataclass
+class H2Storage:
+    nearfield_entries: int
+    farfield_entries: int
+    total_bytes: int
+
+
+def admissible(box_a, box_b, eta):
+    """admissible() on boxes (min xyz, max xyz) (h2.cpp:92-97)."""
+    a = np.ascontiguousarray(box_a, dtype=np.float64)
+    b = np.ascontiguousarray(box_b, dtype=np.float64)
+    return bool(lib().igb_admissible(_p(a), _p(b), float(eta)))
+
+
+class H2Matrix:
+    """H2Matrix<Scalar>(disc, opts) (h2.hpp:57-106), assembled and applied on a B200.
+
+    ``apply(x)`` takes and returns host numpy vectors (float64 for Laplace,
+    complex128 for Helmholtz / Maxwell), like the reference's Eigen vectors."""
+
+    def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int = 0):
+        opts = opts or H2Options()
+        o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
+        h = ctypes.c_void_p()
+        _check(lib().igb_h2_create(disc._h, ctypes.byref(o), int(device), ctypes.byref(h)))
+        self._h = h
+        self._disc = disc
+        self.opts = opts
+        self.dtype = np.complex128 if disc.pde().is_complex() else np.float64
+        n_near, n_far, n_nodes = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_int()
+        _check(lib().igb_h2_counts(h, ctypes.byref(n_near), ctypes.byref(n_far), ctypes.byref(n_nodes)))
+        self.near_count, self.far_count, self.node_count = n_near.value, n_far.value, n_nodes.value
+        self.nch = 4 if disc.pde().is_vector() else 1
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.igb_h2_destroy(self._h)
+            self._h = None
+
+    def rows(self):
+        return self._disc.dof_count()
+
+    cols = rows
+
+    def apply(self, x):
+        x = np.ascontiguousarray(x, dtype=self.dtype)
+        if x.shape != (self.rows(),):
+            raise ValueError("H2Matrix::apply: dimension mismatch")
+        y = np.empty_like(x)
+        _check(lib().igb_h2_apply(self._h, _p(x.view(np.float64)), _p(y.view(np.float64))))
+        return y
+
+    __matmul__ = apply
+    __mul__ = apply
+
+    def apply_device(self, x_ptr: int, y_ptr: int, stream: int = 0):
+        """Device-pointer matvec (x, y: CUDA device addresses of rows() scalars)."""
+        _check(lib().igb_h2_apply_device(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
+                                         ctypes.c_void_p(stream or None)))
+
+    def storage_report(self) -> H2Storage:
+        s = _Storage()
+        _check(lib().igb_h2_storage_report(self._h, ctypes.byref(s)))
+        return H2Storage(s.nearfield_entries, s.farfield_entries, s.total_bytes)
+
+    def nearfield_pairs(self):
+        out = np.zeros((self.near_count, 2), dtype=np.int32)
+        _check(lib().igb_h2_near_pairs(self._h, _p(out, ctypes.c_int)))
+        return out
+
+    def farfield_pairs(self):
+        out = np.zeros((self.far_count, 2), dtype=np.int32)
+        _check(lib().igb_h2_far_pairs(self._h, _p(out, ctypes.c_int)))
+        return out
+
+    def tree(self):
+        n = self.node_count
+        arrs = [np.zeros(n, dtype=np.int32) for _ in range(4)]
+        boxes = np.zeros((n, 6))
+        _check(lib().igb_h2_tree(self._h, *[_p(a, ctypes.c_int) for a in arrs], _p(boxes)))
+        return dict(patch=arrs[0], level=arrs[1], sx=arrs[2], sy=arrs[3], box=boxes)
+
+    # introspection ---------------------------------------------------------
+    def near_blocks(self, first=0, count=None):
+        count = self.near_count - first if count is None else count
+        nl = self._disc.local_count()
+        out = np.zeros((count, nl, nl), dtype=self.dtype)
+        _check(lib().igb_h2_near_blocks(self._h, first, count, _p(out.view(np.float64))))
+        return out
+
+    def couplings(self, first=0, count=None):
+        count = self.far_count - first if count is None else count
+        mm = self.opts.m ** 2
+        out = np.zeros((count, mm, mm), dtype=self.dtype)  # [q][mu][nu]
+        _check(lib().igb_h2_couplings(self._h, first, count, _p(out.view(np.float64))))
+        return np.ascontiguousarray(out.transpose(0, 2, 1))  # [q][nu][mu] = K(nu, mu)
+
+    def moments(self):
+        nl = self._disc.local_count()
+        rows = self.nch * self.opts.m ** 2
+        out = np.zeros((self._disc.element_count(), nl, rows))
+        _check(lib().igb_h2_moments(self._h, _p(out)))
+        return np.ascontiguousarray(out.transpose(0, 2, 1))  # [e][row][l]
+
+    def images(self):
+        out = np.zeros((self.node_count, self.opts.m ** 2, 3))
+        _check(lib().igb_h2_images(self._h, _p(out)))
+        return out
+
+    def assembly_times(self):
+        t = _Times()
+        _check(lib().igb_h2_assembly_times(self._h, ctypes.byref(t)))
+        return {n: getattr(t, n) for n, _ in _Times._fields_}
+
+    def device_bytes(self):
+        a, b, c = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        _check(lib().igb_h2_device_bytes(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return dict(near=a.value, far=b.value, moments=c.value)
+
+    def bench_apply(self, iters):
+        ms = ctypes.c_float()
+        launches = ctypes.c_int()
+        _check(lib().igb_h2_bench_apply(self._h, int(iters), ctypes.byref(ms), ctypes.byref(launches)))
+        return ms.value, launches.value
