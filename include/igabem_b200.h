@@ -141,6 +141,23 @@ int igb_h2_device_bytes(const igb_h2* h, size_t* near, size_t* far, size_t* mome
 /* `iters` back-to-back matvecs on device-resident buffers, CUDA-event timed;
  * *launches = kernels per matvec */
 int igb_h2_bench_apply(igb_h2* h, int iters, float* ms, int* launches);
+/* re-run the device assembly kernels on the resident inputs (benchmark
+ * steps); *device_ms from CUDA events, *launches = kernels launched */
+int igb_h2_reassemble(igb_h2* h, double* device_ms, int* launches);
+/* per-phase matvec time in ms summed over `iters` (event-separated launches):
+ * [coef gather, leaf moments, upward transfer, zero, far couplings, downward
+ * transfer, near rows + leaf backward, DOF scatter] (h2.cpp:271-376) */
+int igb_h2_profile_apply(igb_h2* h, int iters, double phase_ms[8]);
+/* `steps` x (device assembly + `matvecs` matvecs) on the handle stream,
+ * CUDA-event timed; *total_ms, *assembly_ms (sum of assembly device time) */
+int igb_h2_bench_steps(igb_h2* h, int steps, int matvecs, double* total_ms, double* assembly_ms);
+/* unique (ea <= eb) singular work items per class, indexed by IGB_VERTEX,
+ * IGB_EDGE, IGB_COINCIDENT (counts[0] = ordered regular near pairs) */
+int igb_h2_class_counts(const igb_h2* h, long long counts[4]);
+/* kernels per device assembly and per matvec */
+int igb_h2_launch_counts(const igb_h2* h, int* assembly, int* apply);
+/* host->device bytes uploaded by igb_h2_create (geometry tables + plan) */
+int igb_h2_upload_bytes(const igb_h2* h, size_t* bytes);
 void igb_h2_destroy(igb_h2* h);
 
 /* eta-admissibility of two boxes (min xyz, max xyz), h2.cpp:92-97 */

@@ -354,6 +354,51 @@ int igb_h2_bench_apply(igb_h2* h, int iters, float* ms, int* launches) {
     if (launches) *launches = h->dev->apply_kernel_launches();
   });
 }
+int igb_h2_reassemble(igb_h2* h, double* device_ms, int* launches) {
+  return guard([&] {
+    need(h, "h2");
+    const double ms = h->dev->reassemble();
+    if (device_ms) *device_ms = ms;
+    if (launches) *launches = h->dev->assembly_kernel_launches();
+  });
+}
+int igb_h2_profile_apply(igb_h2* h, int iters, double phase_ms[8]) {
+  return guard([&] {
+    need(h, "h2");
+    need(phase_ms, "phase_ms");
+    h->dev->profile_apply(iters, phase_ms);
+  });
+}
+int igb_h2_bench_steps(igb_h2* h, int steps, int matvecs, double* total_ms, double* assembly_ms) {
+  return guard([&] {
+    need(h, "h2");
+    const double t = h->dev->bench_steps(steps, matvecs, assembly_ms);
+    if (total_ms) *total_ms = t;
+  });
+}
+int igb_h2_class_counts(const igb_h2* h, long long counts[4]) {
+  return guard([&] {
+    need(h, "h2");
+    need(counts, "counts");
+    const auto& P = h->dev->plan();
+    counts[0] = static_cast<long long>(P.reg_slot.size());
+    for (int c = 1; c <= 3; ++c) counts[c] = static_cast<long long>(P.sing[c].ea.size());
+  });
+}
+int igb_h2_launch_counts(const igb_h2* h, int* assembly, int* apply) {
+  return guard([&] {
+    need(h, "h2");
+    if (assembly) *assembly = h->dev->assembly_kernel_launches();
+    if (apply) *apply = h->dev->apply_kernel_launches();
+  });
+}
+int igb_h2_upload_bytes(const igb_h2* h, size_t* bytes) {
+  return guard([&] {
+    need(h, "h2");
+    need(bytes, "bytes");
+    *bytes = h->dev->upload_bytes();
+  });
+}
 void igb_h2_destroy(igb_h2* h) { delete h; }
 
 int igb_admissible(const double a[6], const double b[6], double eta) {

@@ -47,6 +47,15 @@ class H2Device {
   double* x_buffer() { return dx_; }
   double* y_buffer() { return dy_; }
   void launch_apply_graph(cudaStream_t s);
+  // re-run the device assembly kernels on the resident inputs; returns device ms
+  double reassemble();
+  // per-phase matvec time (ms summed over iters): coef, leaf_up, upward,
+  // zero, far, downward, near_leaf, scatter
+  void profile_apply(int iters, double* phase_ms);
+  // `steps` x (device assembly + `matvecs` matvecs), CUDA events; returns ms
+  double bench_steps(int steps, int matvecs, double* assembly_ms);
+  int assembly_kernel_launches() const { return assembly_kernels_; }
+  size_t upload_bytes() const { return upload_bytes_; }
   int apply_kernel_launches() const { return apply_launches_; }
 
   // introspection (host copies, reference layouts)
@@ -57,8 +66,9 @@ class H2Device {
 
  private:
   template <class KT> void assemble_impl();
-  template <class KT> void enqueue_apply(const double* x, double* y, cudaStream_t s);
-  void enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s);
+  template <class KT> void run_assembly();
+  template <class KT> void enqueue_apply(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev);
+  void enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev);
 
   std::shared_ptr<const Discretization> disc_;
   H2Plan plan_;
@@ -101,6 +111,15 @@ class H2Device {
   double *h_x_pinned_ = nullptr, *h_y_pinned_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   int apply_launches_ = 0;
+  int assembly_kernels_ = 0, assembly_launches_count_ = 0;
+  size_t upload_bytes_ = 0;
+  struct AsmState {
+    double *gxf = nullptr, *gwf = nullptr, *gxs = nullptr, *gws = nullptr, *lag = nullptr, *cheb = nullptr;
+    int *reg = nullptr, *node_patch = nullptr, *node_level = nullptr, *node_sx = nullptr, *node_sy = nullptr;
+    int* sing[4][4] = {};
+    unsigned char* singm[4][2] = {};
+    double kp[4] = {0, 0, 0, 0};
+  } as_;
 };
 
 }  // namespace igb

@@ -76,7 +76,8 @@ SYMBOLS = (
     "igb_h2_dim", "igb_h2_apply", "igb_h2_apply_device", "igb_h2_storage_report", "igb_h2_counts",
     "igb_h2_near_pairs", "igb_h2_far_pairs", "igb_h2_tree", "igb_h2_near_blocks", "igb_h2_couplings",
     "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
-    "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
+    "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
+    "igb_h2_class_counts", "igb_h2_launch_counts", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
 )
 
 
@@ -123,6 +124,12 @@ def lib():
     L.igb_h2_assembly_times.argtypes = [vp, P(_Times)]
     L.igb_h2_device_bytes.argtypes = [vp, P(sz), P(sz), P(sz)]
     L.igb_h2_bench_apply.argtypes = [vp, i32, P(ctypes.c_float), P(i32)]
+    L.igb_h2_reassemble.argtypes = [vp, P(f64), P(i32)]
+    L.igb_h2_upload_bytes.argtypes = [vp, P(sz)]
+    L.igb_h2_profile_apply.argtypes = [vp, i32, P(f64)]
+    L.igb_h2_class_counts.argtypes = [vp, P(i64)]
+    L.igb_h2_launch_counts.argtypes = [vp, P(i32), P(i32)]
+    L.igb_h2_bench_steps.argtypes = [vp, i32, i32, P(f64), P(f64)]
     L.igb_h2_destroy.argtypes = [vp]
     L.igb_h2_destroy.restype = None
     L.igb_admissible.argtypes = [P(f64), P(f64), f64]
@@ -427,6 +434,42 @@ class H2Matrix:
         a, b, c = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
         _check(lib().igb_h2_device_bytes(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         return dict(near=a.value, far=b.value, moments=c.value)
+
+    def reassemble(self):
+        """Re-run the device assembly kernels (benchmark steps); returns (device ms, kernel launches)."""
+        ms, n = ctypes.c_double(), ctypes.c_int()
+        _check(lib().igb_h2_reassemble(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    PHASES = ("coef", "leaf_up", "upward", "zero", "far", "downward", "near_leaf", "scatter")
+
+    def profile_apply(self, iters=10):
+        """Per-phase matvec device time (ms, summed over iters)."""
+        out = np.zeros(8)
+        _check(lib().igb_h2_profile_apply(self._h, int(iters), _p(out)))
+        return dict(zip(self.PHASES, out.tolist()))
+
+    def bench_steps(self, steps, matvecs):
+        """steps x (device assembly + matvecs matvecs): (total ms, assembly ms) from CUDA events."""
+        t, a = ctypes.c_double(), ctypes.c_double()
+        _check(lib().igb_h2_bench_steps(self._h, int(steps), int(matvecs), ctypes.byref(t), ctypes.byref(a)))
+        return t.value, a.value
+
+    def class_counts(self):
+        """{'regular': ordered regular near pairs, 'vertex'/'edge'/'coincident': unique singular pairs}"""
+        out = np.zeros(4, dtype=np.int64)
+        _check(lib().igb_h2_class_counts(self._h, _p(out, ctypes.c_longlong)))
+        return dict(regular=int(out[0]), vertex=int(out[1]), edge=int(out[2]), coincident=int(out[3]))
+
+    def launch_counts(self):
+        a, b = ctypes.c_int(), ctypes.c_int()
+        _check(lib().igb_h2_launch_counts(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def upload_bytes(self):
+        b = ctypes.c_size_t()
+        _check(lib().igb_h2_upload_bytes(self._h, ctypes.byref(b)))
+        return b.value
 
     def bench_apply(self, iters):
         ms = ctypes.c_float()
