@@ -7,7 +7,7 @@ import io
 import subprocess
 import sys
 
-UNITS = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+UNITS = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}
 
 
 def launches(path):
