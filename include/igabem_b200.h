@@ -160,6 +160,24 @@ int igb_h2_launch_counts(const igb_h2* h, int* assembly, int* apply);
 int igb_h2_upload_bytes(const igb_h2* h, size_t* bytes);
 void igb_h2_destroy(igb_h2* h);
 
+/* ---- host-only block partition (no device): the cluster tree, dual
+ * traversal and pair classification of H2Matrix (h2.cpp:49-97,175-252) ---- */
+typedef struct igb_plan igb_plan;
+int igb_plan_create(const igb_discretization* d, const igb_h2_opts* opts, igb_plan** out);
+int igb_plan_counts(const igb_plan* p, long long* n_near, long long* n_far, int* n_nodes);
+int igb_plan_near_pairs(const igb_plan* p, int* out);
+int igb_plan_far_pairs(const igb_plan* p, int* out);
+/* counts[0] = ordered regular near pairs, counts[1..3] = unique singular
+ * pairs (vertex, edge, coincident) */
+int igb_plan_class_counts(const igb_plan* p, long long counts[4]);
+/* row-cluster partition over `world` ranks: rank owns the contiguous range
+ * [*c0, *c1) of level-1 clusters (cluster = 4*patch + sx + 2*sy), i.e. the
+ * block rows of their leaf elements; reports owned elements and the near /
+ * far pairs whose test element / target node lies in them */
+int igb_plan_partition(const igb_plan* p, int world, int rank, int* c0, int* c1, int* n_elements,
+                       long long* n_near, long long* n_far);
+void igb_plan_destroy(igb_plan* p);
+
 /* eta-admissibility of two boxes (min xyz, max xyz), h2.cpp:92-97 */
 int igb_admissible(const double box_a[6], const double box_b[6], double eta);
 int igb_last_error(char* buf, size_t n);

@@ -19,6 +19,10 @@ struct igb_discretization {
 struct igb_h2 {
   std::unique_ptr<igb::H2Device> dev;
 };
+struct igb_plan {
+  std::shared_ptr<const igb::Discretization> d;
+  igb::H2Plan plan;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -400,6 +404,67 @@ int igb_h2_upload_bytes(const igb_h2* h, size_t* bytes) {
   });
 }
 void igb_h2_destroy(igb_h2* h) { delete h; }
+
+int igb_plan_create(const igb_discretization* d, const igb_h2_opts* opts, igb_plan** out) {
+  return guard([&] {
+    need(d, "discretization");
+    need(out, "out");
+    igb_h2_opts o = opts ? *opts : igb_h2_opts{8, 1.6, 0, 0};
+    auto p = std::make_unique<igb_plan>();
+    p->d = d->d;
+    p->plan = igb::build_plan(*d->d, o.m, o.eta, o.far_order, o.sing_order);
+    *out = p.release();
+  });
+}
+int igb_plan_counts(const igb_plan* p, long long* n_near, long long* n_far, int* n_nodes) {
+  return guard([&] {
+    need(p, "plan");
+    if (n_near) *n_near = static_cast<long long>(p->plan.near_a.size());
+    if (n_far) *n_far = static_cast<long long>(p->plan.far_a.size());
+    if (n_nodes) *n_nodes = p->plan.n_nodes;
+  });
+}
+int igb_plan_near_pairs(const igb_plan* p, int* out) {
+  return guard([&] {
+    need(p, "plan");
+    need(out, "out");
+    for (size_t i = 0; i < p->plan.near_a.size(); ++i) {
+      out[2 * i] = p->plan.near_a[i];
+      out[2 * i + 1] = p->plan.near_b[i];
+    }
+  });
+}
+int igb_plan_far_pairs(const igb_plan* p, int* out) {
+  return guard([&] {
+    need(p, "plan");
+    need(out, "out");
+    for (size_t i = 0; i < p->plan.far_a.size(); ++i) {
+      out[2 * i] = p->plan.far_a[i];
+      out[2 * i + 1] = p->plan.far_b[i];
+    }
+  });
+}
+int igb_plan_class_counts(const igb_plan* p, long long counts[4]) {
+  return guard([&] {
+    need(p, "plan");
+    need(counts, "counts");
+    counts[0] = static_cast<long long>(p->plan.reg_slot.size());
+    for (int c = 1; c <= 3; ++c) counts[c] = static_cast<long long>(p->plan.sing[c].ea.size());
+  });
+}
+int igb_plan_partition(const igb_plan* p, int world, int rank, int* c0, int* c1, int* n_elements,
+                       long long* n_near, long long* n_far) {
+  return guard([&] {
+    need(p, "plan");
+    const auto r = igb::partition_rows(*p->d, p->plan, world, rank);
+    if (c0) *c0 = r.c0;
+    if (c1) *c1 = r.c1;
+    if (n_elements) *n_elements = static_cast<int>(r.elements.size());
+    if (n_near) *n_near = r.near_count;
+    if (n_far) *n_far = r.far_count;
+  });
+}
+void igb_plan_destroy(igb_plan* p) { delete p; }
 
 int igb_admissible(const double a[6], const double b[6], double eta) {
   igb::Box A, B;

@@ -1136,4 +1136,35 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
   return P;
 }
 
+int node_cluster(const H2Plan& P, int node) {
+  const int l = P.node_level[node];
+  if (l == 0) return -1;
+  const int sx = P.node_sx[node] >> (l - 1), sy = P.node_sy[node] >> (l - 1);
+  return 4 * P.node_patch[node] + sx + 2 * sy;
+}
+
+RowPartition partition_rows(const Discretization& d, const H2Plan& P, int world, int rank) {
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("partition: bad rank/world");
+  RowPartition r;
+  const int ncl = d.level() >= 1 ? 4 * P.n_patches : 1;
+  r.c0 = static_cast<int>(static_cast<long long>(ncl) * rank / world);
+  r.c1 = static_cast<int>(static_cast<long long>(ncl) * (rank + 1) / world);
+  const int ne = d.element_count(), n = 1 << d.level();
+  r.owns_element.assign(ne, 0);
+  for (int e = 0; e < ne; ++e) {
+    const Element& el = d.element(e);
+    const int cl = d.level() >= 1 ? 4 * el.patch + (el.ix >= n / 2 ? 1 : 0) + 2 * (el.iy >= n / 2 ? 1 : 0) : 0;
+    if (cl >= r.c0 && cl < r.c1) {
+      r.owns_element[e] = 1;
+      r.elements.push_back(e);
+    }
+  }
+  for (int e : r.elements) r.near_count += P.near_row_start[e + 1] - P.near_row_start[e];
+  for (size_t q = 0; q < P.far_a.size(); ++q) {
+    const int cl = node_cluster(P, P.far_a[q]);
+    if (cl < 0 || (cl >= r.c0 && cl < r.c1)) ++r.far_count;
+  }
+  return r;
+}
+
 }  // namespace igb

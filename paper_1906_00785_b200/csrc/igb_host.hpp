@@ -233,4 +233,17 @@ struct H2Plan {
 };
 H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order);
 
+// Row-cluster partition: rank owns level-1 clusters [c0, c1)
+// (cluster = 4 * patch + sx + 2 * sy); with level 0 the whole operator sits
+// on rank 0.  Far pairs are owned by the rank owning the target's level-1
+// ancestor; level-0 targets are owned by every rank (replicated, tiny).
+struct RowPartition {
+  int c0 = 0, c1 = 0;
+  std::vector<int> elements;          // owned leaf elements, ascending
+  std::vector<unsigned char> owns_element;
+  long long near_count = 0, far_count = 0;
+};
+int node_cluster(const H2Plan& P, int node);  // level-1 cluster of a node, -1 for roots
+RowPartition partition_rows(const Discretization& d, const H2Plan& P, int world, int rank);
+
 }  // namespace igb

@@ -77,7 +77,8 @@ SYMBOLS = (
     "igb_h2_near_pairs", "igb_h2_far_pairs", "igb_h2_tree", "igb_h2_near_blocks", "igb_h2_couplings",
     "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
     "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
-    "igb_h2_class_counts", "igb_h2_launch_counts", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
+    "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_counts", "igb_plan_near_pairs",
+    "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
 )
 
 
@@ -132,6 +133,14 @@ def lib():
     L.igb_h2_bench_steps.argtypes = [vp, i32, i32, P(f64), P(f64)]
     L.igb_h2_destroy.argtypes = [vp]
     L.igb_h2_destroy.restype = None
+    L.igb_plan_create.argtypes = [vp, P(_Opts), P(vp)]
+    L.igb_plan_counts.argtypes = [vp, P(i64), P(i64), P(i32)]
+    L.igb_plan_near_pairs.argtypes = [vp, P(i32)]
+    L.igb_plan_far_pairs.argtypes = [vp, P(i32)]
+    L.igb_plan_class_counts.argtypes = [vp, P(i64)]
+    L.igb_plan_partition.argtypes = [vp, i32, i32, P(i32), P(i32), P(i32), P(i64), P(i64)]
+    L.igb_plan_destroy.argtypes = [vp]
+    L.igb_plan_destroy.restype = None
     L.igb_admissible.argtypes = [P(f64), P(f64), f64]
     L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
     _LIB = L
@@ -328,6 +337,48 @@ def admissible(box_a, box_b, eta):
     a = np.ascontiguousarray(box_a, dtype=np.float64)
     b = np.ascontiguousarray(box_b, dtype=np.float64)
     return bool(lib().igb_admissible(_p(a), _p(b), float(eta)))
+
+
+class H2Plan:
+    """Host-only block partition of H2Matrix (cluster tree, admissibility
+    traversal, pair classification; h2.cpp:49-97,175-252) -- no device."""
+
+    def __init__(self, disc: Discretization, opts: H2Options | None = None):
+        opts = opts or H2Options()
+        o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
+        h = ctypes.c_void_p()
+        _check(lib().igb_plan_create(disc._h, ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+        a, b, c = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_int()
+        _check(lib().igb_plan_counts(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        self.near_count, self.far_count, self.node_count = a.value, b.value, c.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.igb_plan_destroy(self._h)
+            self._h = None
+
+    def nearfield_pairs(self):
+        out = np.zeros((self.near_count, 2), dtype=np.int32)
+        _check(lib().igb_plan_near_pairs(self._h, _p(out, ctypes.c_int)))
+        return out
+
+    def farfield_pairs(self):
+        out = np.zeros((self.far_count, 2), dtype=np.int32)
+        _check(lib().igb_plan_far_pairs(self._h, _p(out, ctypes.c_int)))
+        return out
+
+    def class_counts(self):
+        out = np.zeros(4, dtype=np.int64)
+        _check(lib().igb_plan_class_counts(self._h, _p(out, ctypes.c_longlong)))
+        return dict(regular=int(out[0]), vertex=int(out[1]), edge=int(out[2]), coincident=int(out[3]))
+
+    def partition(self, world, rank):
+        c0, c1, ne = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        nn, nf = ctypes.c_longlong(), ctypes.c_longlong()
+        _check(lib().igb_plan_partition(self._h, int(world), int(rank), ctypes.byref(c0), ctypes.byref(c1),
+                                        ctypes.byref(ne), ctypes.byref(nn), ctypes.byref(nf)))
+        return dict(clusters=(c0.value, c1.value), elements=ne.value, near=nn.value, far=nf.value)
 
 
 class H2Matrix:
