@@ -16,43 +16,69 @@ KIND = {"laplace": 0, "helmholtz": 1, "maxwell": 2}
 FAR, VERTEX, EDGE, COINCIDENT = 0, 1, 2, 3
 
 
+class _Prefixed:
+    """exposes the `ref_*` symbols of oracle/_ref/libigabem_ref.so under the `orc_*` names"""
+
+    def __init__(self, cdll, prefix):
+        self._cdll, self._prefix = cdll, prefix
+
+    def __getattr__(self, name):
+        f = getattr(self._cdll, self._prefix + name[len("orc_"):])
+        setattr(self, name, f)
+        return f
+
+
+def _sig(L, name, argtypes):
+    try:
+        getattr(L, name).argtypes = argtypes
+    except AttributeError:
+        if PREFIX == "orc_":
+            raise  # the restatement must export everything; the reference harness a subset
+
+
+LIB_PATH = os.path.join(_HERE, "liborc.so")
+PREFIX = "orc_"
+
+
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liborc.so")
+        path = LIB_PATH
         if not os.path.exists(path):
-            raise RuntimeError("oracle/liborc.so missing: run `make -C oracle`")
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
         L = ctypes.CDLL(path)
+        if PREFIX != "orc_":
+            L = _Prefixed(L, PREFIX)
         vp, i32, f64, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong
         P = ctypes.POINTER
-        L.orc_disc_create.argtypes = [i32, f64, P(f64), i32, f64, f64, i32, i32, i32, P(vp)]
-        L.orc_disc_destroy.argtypes = [vp]
-        L.orc_disc_info.argtypes = [vp, P(i32)]
-        L.orc_disc_l2g.argtypes = [vp, P(i32), P(f64)]
-        L.orc_disc_elements.argtypes = [vp, P(i32), P(f64)]
-        L.orc_patch.argtypes = [vp, i32, P(i32), P(f64), P(f64), P(f64), P(f64)]
-        L.orc_edges.argtypes = [vp, P(i32)]
-        L.orc_frame.argtypes = [vp, i32, f64, f64, P(f64)]
-        L.orc_sample_shapes.argtypes = [vp, i32, f64, f64, P(f64), P(f64), P(f64)]
-        L.orc_classify.argtypes = [vp, i32, i32, P(i32)]
-        L.orc_pair_blocks.argtypes = [vp, P(i32), i64, i32, i32, P(f64)]
-        L.orc_dense.argtypes = [vp, i32, i32, P(f64)]
-        L.orc_h2_create.argtypes = [vp, i32, f64, i32, i32, i32, P(vp)]
-        L.orc_h2_destroy.argtypes = [vp]
-        L.orc_h2_info.argtypes = [vp, P(i64)]
-        L.orc_h2_near_pairs.argtypes = [vp, P(i32)]
-        L.orc_h2_far_pairs.argtypes = [vp, P(i32)]
-        L.orc_h2_near_blocks.argtypes = [vp, i64, i64, P(f64)]
-        L.orc_h2_couplings.argtypes = [vp, i64, i64, P(f64)]
-        L.orc_h2_moments.argtypes = [vp, P(f64)]
-        L.orc_h2_images.argtypes = [vp, P(f64)]
-        L.orc_h2_boxes.argtypes = [vp, P(f64)]
-        L.orc_h2_transfer.argtypes = [vp, P(f64), P(f64)]
-        L.orc_h2_apply.argtypes = [vp, P(f64), P(f64)]
-        L.orc_gauss.argtypes = [i32, P(f64), P(f64)]
-        L.orc_pair_rule.argtypes = [i32, i32, P(f64), P(i64)]
-        L.orc_admissible.argtypes = [P(f64), P(f64), f64]
-        L.orc_last_error.argtypes = [ctypes.c_char_p, i32]
+        _sig(L, "orc_disc_create", [i32, f64, P(f64), i32, f64, f64, i32, i32, i32, P(vp)])
+        _sig(L, "orc_disc_destroy", [vp])
+        _sig(L, "orc_disc_info", [vp, P(i32)])
+        _sig(L, "orc_disc_l2g", [vp, P(i32), P(f64)])
+        _sig(L, "orc_disc_elements", [vp, P(i32), P(f64)])
+        _sig(L, "orc_patch", [vp, i32, P(i32), P(f64), P(f64), P(f64), P(f64)])
+        _sig(L, "orc_edges", [vp, P(i32)])
+        _sig(L, "orc_frame", [vp, i32, f64, f64, P(f64)])
+        _sig(L, "orc_sample_shapes", [vp, i32, f64, f64, P(f64), P(f64), P(f64)])
+        _sig(L, "orc_classify", [vp, i32, i32, P(i32)])
+        _sig(L, "orc_pair_blocks", [vp, P(i32), i64, i32, i32, P(f64)])
+        _sig(L, "orc_dense", [vp, i32, i32, P(f64)])
+        _sig(L, "orc_h2_create", [vp, i32, f64, i32, i32, i32, P(vp)])
+        _sig(L, "orc_h2_destroy", [vp])
+        _sig(L, "orc_h2_info", [vp, P(i64)])
+        _sig(L, "orc_h2_near_pairs", [vp, P(i32)])
+        _sig(L, "orc_h2_far_pairs", [vp, P(i32)])
+        _sig(L, "orc_h2_near_blocks", [vp, i64, i64, P(f64)])
+        _sig(L, "orc_h2_couplings", [vp, i64, i64, P(f64)])
+        _sig(L, "orc_h2_moments", [vp, P(f64)])
+        _sig(L, "orc_h2_images", [vp, P(f64)])
+        _sig(L, "orc_h2_boxes", [vp, P(f64)])
+        _sig(L, "orc_h2_transfer", [vp, P(f64), P(f64)])
+        _sig(L, "orc_h2_apply", [vp, P(f64), P(f64)])
+        _sig(L, "orc_gauss", [i32, P(f64), P(f64)])
+        _sig(L, "orc_pair_rule", [i32, i32, P(f64), P(i64)])
+        _sig(L, "orc_admissible", [P(f64), P(f64), f64])
+        _sig(L, "orc_last_error", [ctypes.c_char_p, i32])
         _LIB = L
     return _LIB
 

@@ -1,0 +1,59 @@
+"""Generate tests/golden/*.npz from the REFERENCE itself (oracle/_ref, the
+igabem core compiled against the Eigen-subset shim).  Run in this container
+(needs /root/reference at build time only):
+
+    python tools/make_golden.py            # small cases
+    python tools/make_golden.py c2         # full-size c2 matvec (minutes)
+
+Each fixture stores the configuration, the seeded input x
+(uniform[-1,1], numpy default_rng(20261019)), y = H x, partition counts,
+storage report, and near-field blocks of a deterministic sample of pairs."""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle import pyref  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+SMALL = {
+    # name: kind, P, rep, L, m, kappa
+    "c1_laplace_P2_L3_m8": ("laplace", 2, 1, 3, 8, 0.0),
+    "laplace_P3_L3_m4": ("laplace", 3, 1, 3, 4, 0.0),
+    "laplace_P4_L2_m5": ("laplace", 4, 1, 2, 5, 0.0),
+    "laplace_P0_L3_m4": ("laplace", 0, 1, 3, 4, 0.0),
+    "helmholtz_P3_L2_m8_k4pi": ("helmholtz", 3, 1, 2, 8, 4 * np.pi),
+    "maxwell_P2_L2_m8_k2pi": ("maxwell", 2, 1, 2, 8, 2 * np.pi),
+}
+BIG = {"c2_laplace_P3_L6_m4": ("laplace", 3, 1, 6, 4, 0.0)}
+
+
+def make(name, cfg, nblocks=400):
+    kind, P, rep, L, m, kappa = cfg
+    t0 = time.time()
+    d = pyref.Discretization(kind, P, rep, L, kappa=kappa)
+    h = pyref.H2Matrix(d, m=m, eta=1.6)
+    rng = np.random.default_rng(20261019)
+    x = rng.uniform(-1, 1, d.dof_count)
+    if d.is_complex:
+        x = x + 1j * rng.uniform(-1, 1, d.dof_count)
+    y = h.apply(x)
+    near = h.nearfield_pairs()
+    idx = np.linspace(0, len(near) - 1, min(nblocks, len(near))).astype(np.int64)
+    blocks = d.pair_blocks(near[idx])
+    np.savez_compressed(os.path.join(OUT, name + ".npz"), kind=kind, P=P, rep=rep, L=L, m=m, eta=1.6,
+                        kappa=kappa, x=x, y=y, near_count=h.near_count, far_count=h.far_count,
+                        nearfield_entries=h.nearfield_entries, farfield_entries=h.farfield_entries,
+                        total_bytes=h.total_bytes, block_pairs=near[idx], blocks=blocks,
+                        generator="oracle/_ref (reference igabem core + Eigen-subset shim)")
+    print(f"{name}: dofs={d.dof_count} near={h.near_count} far={h.far_count} {time.time() - t0:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    which = BIG if len(sys.argv) > 1 and sys.argv[1] == "c2" else SMALL
+    for name, cfg in which.items():
+        make(name, cfg)
