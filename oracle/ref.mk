@@ -19,3 +19,9 @@ _ref/libigabem_ref.so: $(OBJS)
 clean:
 	rm -rf _ref
 .PHONY: all clean
+
+# C++ drop-in test program: reference headers + shim + include/igabem_b200
+../tests/cpp/dropin_test: ../tests/cpp/dropin_test.cpp ../include/igabem_b200/h2_dropin.hpp _ref/libigabem_ref.so
+	$(CXX) $(CXXFLAGS) -I../include $< -o $@ -L_ref -ligabem_ref -L../paper_1906_00785_b200 -ligabem_b200 \
+	  -Wl,-rpath,'$$ORIGIN/../../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../../paper_1906_00785_b200'
+all: ../tests/cpp/dropin_test

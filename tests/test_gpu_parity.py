@@ -121,3 +121,17 @@ def test_errors(igb):
     h = igb.H2Matrix(d, igb.H2Options(m=4))
     with pytest.raises(ValueError):
         h.apply(np.zeros(d.dof_count() + 1))
+
+
+def test_cpp_dropin_against_reference():
+    """C++ code written against the reference API (igabem::Discretization,
+    H2Options) swaps igabem::H2Matrix for igabem_b200::H2Matrix and gets the
+    same partition, storage report and matvec (tests/cpp/dropin_test.cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_test not built (needs /root/reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
