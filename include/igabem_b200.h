@@ -99,6 +99,11 @@ typedef struct {
 /* H2Matrix<Scalar>(disc, opts)  h2.hpp:60, h2.cpp:99-129: full assembly on
  * CUDA device `device`.  The discretization may be destroyed afterwards. */
 int igb_h2_create(const igb_discretization* d, const igb_h2_opts* opts, int device, igb_h2** out);
+/* flags for igb_h2_create_ex: IGB_H2_STORED_COUPLINGS keeps the far couplings
+ * in HBM in the reference format (h2.cpp:218-229); the default evaluates them
+ * on the fly inside the matvec (same values, no coupling storage) */
+enum { IGB_H2_STORED_COUPLINGS = 2 };
+int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, igb_h2** out);
 /* rows()/cols()  h2.hpp:62-63 */
 int igb_h2_dim(const igb_h2* h, int* rows);
 /* apply(x) / operator*  h2.hpp:64-69, h2.cpp:254-378: host buffers of rows()

@@ -197,6 +197,14 @@ int igb_h2_create(const igb_discretization* d, const igb_h2_opts* opts, int devi
     *out = new igb_h2{std::make_unique<igb::H2Device>(d->d, o.m, o.eta, o.far_order, o.sing_order, device)};
   });
 }
+int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, igb_h2** out) {
+  return guard([&] {
+    need(d, "discretization");
+    need(out, "out");
+    igb_h2_opts o = opts ? *opts : igb_h2_opts{8, 1.6, 0, 0};
+    *out = new igb_h2{std::make_unique<igb::H2Device>(d->d, o.m, o.eta, o.far_order, o.sing_order, device, flags)};
+  });
+}
 int igb_h2_dim(const igb_h2* h, int* rows) {
   return guard([&] {
     need(h, "h2");

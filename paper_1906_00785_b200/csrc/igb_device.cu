@@ -852,6 +852,250 @@ __global__ void __launch_bounds__(256) k_far(int n_targets, const int* __restric
   }
 }
 
+// Fused far field: couplings evaluated on the fly from the L2-resident node
+// images, K_q[nu][mu] = G(|img_t[nu] - img_s[mu]|) (h2.cpp:218-229), applied
+// as in h2.cpp:312-326.  One warp per target; G lane groups take alternate
+// source clusters; each source's images + moments are staged once per warp in
+// shared memory and read back as broadcasts.  No coupling bytes touch HBM.
+template <class KT, int R>
+__global__ void __launch_bounds__(256) k_far_fused(int n_targets, const int* __restrict__ targets,
+                                                   const int* __restrict__ far_rs, const int* __restrict__ far_b,
+                                                   const double* __restrict__ img, int mm,
+                                                   const typename KT::S* __restrict__ up, KParams kp,
+                                                   typename KT::S* __restrict__ down) {
+  using S = typename KT::S;
+  constexpr int NCH = KT::NC;
+  constexpr int SW = sizeof(S) / 8;
+  constexpr int PW = ((4 + NCH * SW) + 1) / 2 * 2;  // x, y, z, pad, moments; even => 16 B aligned
+  extern __shared__ __align__(16) double smf[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double* wsm = smf + static_cast<size_t>(wib) * 32 * R * PW;
+  if (warp >= n_targets) return;
+  const int t = targets[warp];
+  const int rows = NCH * mm;
+  const int G = (mm <= 32) ? 32 / mm : 1;
+  const int g = (mm <= 32) ? lane / mm : 0;
+  const int lig = (mm <= 32) ? lane % mm : lane;  // lane index within the group
+  const bool ok = g < G;
+  double* gsm = wsm + static_cast<size_t>(g < G ? g : 0) * mm * PW;
+  double tx[R][3];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int nu = lig + 32 * r;
+    const double* p = img + (static_cast<size_t>(t) * mm + (nu < mm ? nu : 0)) * 3;
+    tx[r][0] = p[0];
+    tx[r][1] = p[1];
+    tx[r][2] = p[2];
+  }
+  S acc[NCH][R];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[c][r] = zero<S>();
+  const int q0 = far_rs[t], q1 = far_rs[t + 1];
+  for (int base = q0; base < q1; base += G) {
+    const int q = base + g;
+    const bool valid = ok && q < q1;
+    if (valid) {
+      const int s = far_b[q];
+      const double* is = img + static_cast<size_t>(s) * mm * 3;
+      const S* us = up + static_cast<size_t>(s) * rows;
+      for (int mu = lig; mu < mm; mu += (mm <= 32 ? mm : 32)) {
+        double* d = gsm + mu * PW;
+        d[0] = is[3 * mu];
+        d[1] = is[3 * mu + 1];
+        d[2] = is[3 * mu + 2];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) reinterpret_cast<S*>(d + 4)[c] = us[c * mm + mu];
+      }
+    }
+    __syncwarp();
+    if (valid) {
+      S part[NCH][R];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int r = 0; r < R; ++r) part[c][r] = zero<S>();
+#pragma unroll 2
+      for (int mu = 0; mu < mm; ++mu) {
+        const double* d = gsm + mu * PW;
+        const double2 xy = *reinterpret_cast<const double2*>(d);
+        const double sz = d[2];
+        S xv[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) xv[c] = reinterpret_cast<const S*>(d + 4)[c];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double d0 = tx[r][0] - xy.x, d1 = tx[r][1] - xy.y, d2 = tx[r][2] - sz;
+          const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) fmac(part[c][r], gk, xv[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if constexpr (NCH == 4) {
+            if (c == 3) {
+              acc[c][r] = acc[c][r] + part[c][r] * mk(kp.dwx, kp.dwy);
+              continue;
+            }
+          }
+          acc[c][r] = acc[c][r] + part[c][r];
+        }
+    }
+    __syncwarp();
+  }
+  for (int gg = 1; gg < G; ++gg) {
+    const int src = (lane + gg * mm < 32) ? lane + gg * mm : lane;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      const S v = shfl_idx(acc[c][0], src);
+      if (g == 0) acc[c][0] = acc[c][0] + v;
+    }
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int nu = lig + 32 * r;
+      if (nu < mm)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) down[static_cast<size_t>(t) * rows + c * mm + nu] = acc[c][r];
+    }
+  }
+}
+
+// Branch-free FP64 reciprocal square root for normal positive inputs:
+// MUFU.RSQ64H seed (rsqrt.approx.ftz.f64, rel. err < 2^-22) + 2 Newton steps.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+template <int M>
+struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
+  static constexpr int MM = M * M;
+  static constexpr int BR = (M == 3) ? 3 : (M == 5 ? 5 : 4);
+  static constexpr int BC = (M == 2) ? 4 : (M == 3 ? 9 : (M == 5 ? 6 : 8));
+  static constexpr int RN = (MM + BR - 1) / BR, CN = (MM + BC - 1) / BC;
+  static_assert(BR * BC <= 32, "lane grid");
+};
+
+// Symmetric fused far field (Laplace): each unordered admissible pair {t, s},
+// t < s, is evaluated once by the warp of t: K = G(|img_t[nu] - img_s[mu]|)
+// gives down[t] += K up[s] (accumulated in registers) and K^T up[t], written to
+// the slot of the transposed pair (s, t) and summed by k_far_lower in fixed
+// order.  Lane (bi, bj) owns RN target rows x CN source columns.
+template <int M>
+__global__ void __launch_bounds__(256) k_far_sym(int n_targets, const int* __restrict__ targets,
+                                                 const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+                                                 const int* __restrict__ far_b, const int* __restrict__ trans,
+                                                 const double* __restrict__ img, const double* __restrict__ up,
+                                                 double* __restrict__ down, double* __restrict__ slot) {
+  using T = SymTile<M>;
+  constexpr int MM = T::MM, BR = T::BR, BC = T::BC, RN = T::RN, CN = T::CN;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_targets) return;
+  const int t = targets[warp];
+  const int bi = lane % BR, bj = lane / BR;
+  const bool act = bj < BC;
+  double tx[RN][3], xt[RN], acc[RN];
+#pragma unroll
+  for (int i = 0; i < RN; ++i) {
+    const int nu = bi + BR * i;
+    const bool ok = act && nu < MM;
+    const double* p = img + (static_cast<size_t>(t) * MM + (ok ? nu : 0)) * 3;
+    tx[i][0] = p[0];
+    tx[i][1] = p[1];
+    tx[i][2] = p[2];
+    xt[i] = ok ? up[static_cast<size_t>(t) * MM + nu] : 0.0;
+    acc[i] = 0.0;
+  }
+  const int q0 = upper_start[t], q1 = far_rs[t + 1];
+  for (int q = q0; q < q1; ++q) {
+    const int s = far_b[q];
+    double sx[CN][3], xs[CN], ps[CN];
+#pragma unroll
+    for (int j = 0; j < CN; ++j) {
+      const int mu = bj + BC * j;
+      const bool ok = act && mu < MM;
+      const double* p = img + (static_cast<size_t>(s) * MM + (ok ? mu : 0)) * 3;
+      sx[j][0] = __ldg(p);
+      sx[j][1] = __ldg(p + 1);
+      sx[j][2] = __ldg(p + 2);
+      xs[j] = ok ? __ldg(up + static_cast<size_t>(s) * MM + mu) : 0.0;
+      ps[j] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < RN; ++i)
+#pragma unroll
+      for (int j = 0; j < CN; ++j) {
+        const double d0 = tx[i][0] - sx[j][0], d1 = tx[i][1] - sx[j][1], d2 = tx[i][2] - sx[j][2];
+        const double gk = rsqrt_nr(d0 * d0 + d1 * d1 + d2 * d2);  // 4 pi G
+        acc[i] = fma(gk, xs[j], acc[i]);
+        ps[j] = fma(gk, xt[i], ps[j]);
+      }
+    // K^T up[t] for the CN columns: reduce over the BR lanes of the column
+#pragma unroll
+    for (int j = 0; j < CN; ++j) {
+      double v = ps[j];
+#pragma unroll
+      for (int o = 1; o < BR; o <<= 1) {
+        const double w = __shfl_down_sync(0xffffffffu, v, o);
+        if (bi + o < BR) v += w;
+      }
+      ps[j] = v;
+    }
+    if (act && bi == 0) {
+      double* dst = slot + static_cast<size_t>(trans[q]) * MM;
+#pragma unroll
+      for (int j = 0; j < CN; ++j) {
+        const int mu = bj + BC * j;
+        if (mu < MM) dst[mu] = ps[j] * kInv4Pi;
+      }
+    }
+  }
+  // K up[s] summed over the warp's sources: reduce over the BC lanes of the row
+#pragma unroll
+  for (int i = 0; i < RN; ++i) {
+    double v = acc[i];
+#pragma unroll
+    for (int o = 1; o < BC; o <<= 1) {
+      const double w = __shfl_down_sync(0xffffffffu, v, o * BR);
+      if (bj + o < BC) v += w;
+    }
+    acc[i] = v;
+  }
+  if (bj == 0) {
+#pragma unroll
+    for (int i = 0; i < RN; ++i) {
+      const int nu = bi + BR * i;
+      if (nu < MM) down[static_cast<size_t>(t) * MM + nu] = acc[i] * kInv4Pi;
+    }
+  }
+}
+
+// down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
+// in ascending t (fixed order)
+__global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs, const int* __restrict__ upper_start,
+                            const double* __restrict__ slot, double* __restrict__ down) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n_nodes) * mm) return;
+  const int s = static_cast<int>(idx / mm), nu = static_cast<int>(idx % mm);
+  const int q0 = far_rs[s], q1 = upper_start[s];
+  if (q0 == q1) return;
+  double acc = down[idx];
+  for (int q = q0; q < q1; ++q) acc += slot[static_cast<size_t>(q) * mm + nu];
+  down[idx] = acc;
+}
+
 // child(i,j) += tu^T X tv  (h2.cpp:328-347)
 template <class S>
 __global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, int m, int nch,
@@ -1089,6 +1333,18 @@ void H2Device::assemble_impl() {
       if (P.far_row_start[t + 1] > P.far_row_start[t]) targets.push_back(t);
     n_far_targets_ = static_cast<int>(targets.size());
     d_far_targets_ = upload(targets);
+    // symmetric fused far field (Laplace, m <= 6): upper pairs + transposes
+    sym_far_ = !stored_couplings() && d.kind() == kLaplace && m >= 2 && m <= 6;
+    if (sym_far_) {
+      std::vector<int> sym_targets;
+      for (int t = 0; t < P.n_nodes; ++t)
+        if (P.far_upper_start[t] < P.far_row_start[t + 1]) sym_targets.push_back(t);
+      n_sym_targets_ = static_cast<int>(sym_targets.size());
+      d_sym_targets_ = upload(sym_targets);
+      d_upper_start_ = upload(P.far_upper_start);
+      d_trans_ = upload(P.far_trans);
+      d_slot_ = dalloc<double>(P.far_a.size() * static_cast<size_t>(mm));
+    }
   }
   d_dof_start_ = upload(P.dof_start);
   d_dof_inc_ = upload(P.dof_inc);
@@ -1139,13 +1395,13 @@ void H2Device::assemble_impl() {
   const long long nfarp = static_cast<long long>(P.far_a.size());
   const int nf = P.nfar, nq = nf * nf;
   d_near_ = dalloc<double>(static_cast<size_t>(nnear) * NL * NL * sw);
-  d_far_ = dalloc<double>(static_cast<size_t>(nfarp) * mm * mm * sw);
+  if (stored_couplings()) d_far_ = dalloc<double>(static_cast<size_t>(nfarp) * mm * mm * sw);
   d_mom_ = dalloc<double>(static_cast<size_t>(ne) * NL * rows);
   d_img_ = dalloc<double>(static_cast<size_t>(P.n_nodes) * mm * 3);
   d_cpts_ = dalloc<double>(static_cast<size_t>(ne) * nq * 3);
   d_cval_ = dalloc<double>(static_cast<size_t>(ne) * NC * nq * NL);
   bytes_.near = static_cast<size_t>(nnear) * NL * NL * 8 * sw;
-  bytes_.far = static_cast<size_t>(nfarp) * mm * mm * 8 * sw;
+  bytes_.far = stored_couplings() ? static_cast<size_t>(nfarp) * mm * mm * 8 * sw : 0;
   bytes_.moments = static_cast<size_t>(ne) * NL * rows * 8;
   IGB_CUDA(cudaEventRecord(ev[1], stream_));
   IGB_CUDA(cudaStreamSynchronize(stream_));
@@ -1162,6 +1418,9 @@ void H2Device::assemble_impl() {
   d_down_ = dalloc<double>(nn * rows * sw);
   d_loc_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
   IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaStreamSynchronize(stream_));
   for (auto& e : ev) cudaEventDestroy(e);
 }
@@ -1230,8 +1489,8 @@ void H2Device::run_assembly() {
     IGB_CUDA(cudaGetLastError());
   }
   IGB_CUDA(cudaEventRecord(ev[3], stream_));
-  // ---- K3 couplings
-  if (nfarp > 0) {
+  // ---- K3 couplings (stored mode only; fused mode evaluates them in the matvec)
+  if (nfarp > 0 && stored_couplings()) {
     k_couplings<KT><<<148 * 16, 256, 0, stream_>>>(nfarp, mm, d_far_a_, d_far_b_, d_img_, kp, d_far_);
     ++launched;
     IGB_CUDA(cudaGetLastError());
@@ -1371,24 +1630,56 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
   ++launches;
   mark(4);
   if (n_far_targets_ > 0) {
-    S dw;
-    if constexpr (sizeof(S) == 8) {
-      dw = 1.0;
-    } else {
-      const cplx kap = d.kappa();
-      const cplx w = d.is_vector() ? -1.0 / (kap * kap) : cplx(1.0, 0.0);
-      dw = mk(w.real(), w.imag());
-    }
     const unsigned grid = grid_for(static_cast<long long>(n_far_targets_) * 32, 256);
-    const S* K = reinterpret_cast<const S*>(d_far_);
-    if (nch_ == 4) {
-      if (mm <= 32) k_far<S, 4, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-      else if (mm <= 64) k_far<S, 4, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-      else k_far<S, 4, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+    if (stored_couplings()) {
+      S dw;
+      if constexpr (sizeof(S) == 8) {
+        dw = 1.0;
+      } else {
+        const cplx kap = d.kappa();
+        const cplx w = d.is_vector() ? -1.0 / (kap * kap) : cplx(1.0, 0.0);
+        dw = mk(w.real(), w.imag());
+      }
+      const S* K = reinterpret_cast<const S*>(d_far_);
+      if (nch_ == 4) {
+        if (mm <= 32) k_far<S, 4, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else if (mm <= 64) k_far<S, 4, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else k_far<S, 4, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+      } else {
+        if (mm <= 32) k_far<S, 1, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else if (mm <= 64) k_far<S, 1, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else k_far<S, 1, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+      }
+    } else if (sym_far_) {
+      const unsigned gsym = grid_for(static_cast<long long>(n_sym_targets_) * 32, 256);
+      double* dn = reinterpret_cast<double*>(down);
+      const double* upd = reinterpret_cast<const double*>(up);
+      switch (m) {
+        case 2: k_far_sym<2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        case 3: k_far_sym<3><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        case 4: k_far_sym<4><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        case 5: k_far_sym<5><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        default: k_far_sym<6><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+      }
+      ++launches;
+      k_far_lower<<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(P.n_nodes, mm, d_far_rs_, d_upper_start_, d_slot_, dn);
     } else {
-      if (mm <= 32) k_far<S, 1, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-      else if (mm <= 64) k_far<S, 1, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-      else k_far<S, 1, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+      KParams kp;
+      kp.kr = as_.kp[0];
+      kp.ki = as_.kp[1];
+      kp.dwx = as_.kp[2];
+      kp.dwy = as_.kp[3];
+      constexpr int PW = ((4 + KT::NC * static_cast<int>(sizeof(S) / 8)) + 1) / 2 * 2;
+      if (mm <= 32) {
+        const size_t smem = 8 * 32 * 1 * PW * 8;
+        k_far_fused<KT, 1><<<grid, 256, smem, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, d_img_, mm, up, kp, down);
+      } else if (mm <= 64) {
+        const size_t smem = 8 * 32 * 2 * PW * 8;
+        k_far_fused<KT, 2><<<grid, 256, smem, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, d_img_, mm, up, kp, down);
+      } else {
+        const size_t smem = 8 * 32 * 4 * PW * 8;
+        k_far_fused<KT, 4><<<grid, 256, smem, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, d_img_, mm, up, kp, down);
+      }
     }
     ++launches;
   }
@@ -1544,7 +1835,29 @@ void H2Device::couplings(long long first, long long count, double* out) const {
   if (first < 0 || first + count > static_cast<long long>(plan_.far_a.size()))
     throw std::invalid_argument("couplings: range out of bounds");
   IGB_CUDA(cudaSetDevice(device_));
-  IGB_CUDA(cudaMemcpy(out, d_far_ + first * per, count * per * 8, cudaMemcpyDeviceToHost));
+  if (count == 0) return;
+  if (d_far_) {
+    IGB_CUDA(cudaMemcpy(out, d_far_ + first * per, count * per * 8, cudaMemcpyDeviceToHost));
+    return;
+  }
+  // fused mode: evaluate the requested couplings with the assembly kernel
+  double* tmp = nullptr;
+  IGB_CUDA(cudaMalloc(&tmp, count * per * 8));
+  KParams kp;
+  kp.kr = as_.kp[0];
+  kp.ki = as_.kp[1];
+  kp.dwx = as_.kp[2];
+  kp.dwy = as_.kp[3];
+  const int mm = plan_.m * plan_.m;
+  if (is_complex())
+    k_couplings<HelmT<0>><<<148 * 16, 256, 0, stream_>>>(count, mm, d_far_a_ + first, d_far_b_ + first, d_img_, kp, tmp);
+  else
+    k_couplings<LapT<0>><<<148 * 16, 256, 0, stream_>>>(count, mm, d_far_a_ + first, d_far_b_ + first, d_img_, kp, tmp);
+  const cudaError_t e1 = cudaStreamSynchronize(stream_);
+  const cudaError_t e2 = cudaMemcpy(out, tmp, count * per * 8, cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  IGB_CUDA(e1);
+  IGB_CUDA(e2);
 }
 void H2Device::moments(double* out) const {
   IGB_CUDA(cudaSetDevice(device_));

@@ -21,7 +21,8 @@ struct DeviceBytes {
 
 class H2Device {
  public:
-  // flags bit0: keep the element quadrature caches resident (introspection)
+  // flags bit1 (IGB_H2_STORED_COUPLINGS): store the far couplings (reference
+  // format) instead of evaluating them inside the matvec
   H2Device(std::shared_ptr<const Discretization> d, int m, double eta, int far_order,
            int sing_order, int device, int flags = 0);
   ~H2Device();
@@ -29,6 +30,7 @@ class H2Device {
   H2Device& operator=(const H2Device&) = delete;
 
   const Discretization& disc() const { return *disc_; }
+  bool stored_couplings() const { return (flags_ & 2) != 0; }
   const H2Plan& plan() const { return plan_; }
   bool is_complex() const { return disc_->is_complex(); }
   int dim() const { return disc_->dof_count(); }
@@ -95,6 +97,10 @@ class H2Device {
   int *d_near_a_ = nullptr, *d_near_b_ = nullptr, *d_near_rs_ = nullptr;
   int *d_far_b_ = nullptr, *d_far_rs_ = nullptr, *d_far_targets_ = nullptr;
   int n_far_targets_ = 0;
+  bool sym_far_ = false;
+  int n_sym_targets_ = 0;
+  int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;
+  double* d_slot_ = nullptr;
   int *d_far_a_ = nullptr;
   int *d_dof_start_ = nullptr, *d_dof_inc_ = nullptr;
   double *d_tl_ = nullptr, *d_tr_ = nullptr;

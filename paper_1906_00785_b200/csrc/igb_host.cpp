@@ -1073,6 +1073,26 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
   P.far_row_start.assign(nn + 1, 0);
   for (long long q = 0; q < nfar_pairs; ++q) ++P.far_row_start[P.far_a[q] + 1];
   for (int t = 0; t < nn; ++t) P.far_row_start[t + 1] += P.far_row_start[t];
+  // symmetric structure of the admissible pairs: (t, s) <-> (s, t)
+  P.far_upper_start.resize(nn);
+  P.far_trans.assign(nfar_pairs, -1);
+  int asym = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : asym)
+  for (int t = 0; t < nn; ++t) {
+    const auto first = P.far_b.begin() + P.far_row_start[t], last = P.far_b.begin() + P.far_row_start[t + 1];
+    P.far_upper_start[t] = static_cast<int>(std::upper_bound(first, last, t) - P.far_b.begin());
+    for (int q = P.far_row_start[t]; q < P.far_row_start[t + 1]; ++q) {
+      const int s = P.far_b[q];
+      const auto f2 = P.far_b.begin() + P.far_row_start[s], l2 = P.far_b.begin() + P.far_row_start[s + 1];
+      const auto it = std::lower_bound(f2, l2, t);
+      if (it == l2 || *it != t) {
+        ++asym;
+        continue;
+      }
+      P.far_trans[q] = static_cast<int>(it - P.far_b.begin());
+    }
+  }
+  if (asym) throw std::logic_error("B200 H2: admissible relation is not symmetric");
 
   // classification + unique singular work lists
   P.near_cls.resize(nnear);

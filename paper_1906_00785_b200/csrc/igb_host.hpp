@@ -211,6 +211,8 @@ struct H2Plan {
   std::vector<int> far_a, far_b;    // node pairs, sorted by (a, b)
   std::vector<int> near_row_start;  // ne + 1
   std::vector<int> far_row_start;   // n_nodes + 1
+  std::vector<int> far_upper_start; // per node: first pair (t, s) of row t with s > t
+  std::vector<int> far_trans;       // per pair (t, s): index of (s, t)
   // near pair classification
   std::vector<uint8_t> near_cls;
   // unique singular work items per class (ea <= eb): element ids, map bits,

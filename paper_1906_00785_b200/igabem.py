@@ -72,7 +72,7 @@ class _PatchDesc(ctypes.Structure):
 SYMBOLS = (
     "igb_geometry_create", "igb_geometry_sphere", "igb_geometry_square", "igb_geometry_info",
     "igb_geometry_destroy", "igb_discretization_create", "igb_discretization_info", "igb_discretization_l2g",
-    "igb_discretization_elements", "igb_classify_pair", "igb_discretization_destroy", "igb_h2_create",
+    "igb_discretization_elements", "igb_classify_pair", "igb_discretization_destroy", "igb_h2_create", "igb_h2_create_ex",
     "igb_h2_dim", "igb_h2_apply", "igb_h2_apply_device", "igb_h2_storage_report", "igb_h2_counts",
     "igb_h2_near_pairs", "igb_h2_far_pairs", "igb_h2_tree", "igb_h2_near_blocks", "igb_h2_couplings",
     "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
@@ -110,6 +110,7 @@ def lib():
     L.igb_discretization_destroy.argtypes = [vp]
     L.igb_discretization_destroy.restype = None
     L.igb_h2_create.argtypes = [vp, P(_Opts), i32, P(vp)]
+    L.igb_h2_create_ex.argtypes = [vp, P(_Opts), i32, i32, P(vp)]
     L.igb_h2_dim.argtypes = [vp, P(i32)]
     L.igb_h2_apply.argtypes = [vp, P(f64), P(f64)]
     L.igb_h2_apply_device.argtypes = [vp, vp, vp, vp]
@@ -387,11 +388,14 @@ class H2Matrix:
     ``apply(x)`` takes and returns host numpy vectors (float64 for Laplace,
     complex128 for Helmholtz / Maxwell), like the reference's Eigen vectors."""
 
-    def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int = 0):
+    def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int = 0,
+                 stored_couplings: bool = False):
         opts = opts or H2Options()
         o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
         h = ctypes.c_void_p()
-        _check(lib().igb_h2_create(disc._h, ctypes.byref(o), int(device), ctypes.byref(h)))
+        flags = 2 if stored_couplings else 0
+        _check(lib().igb_h2_create_ex(disc._h, ctypes.byref(o), int(device), flags, ctypes.byref(h)))
+        self.stored_couplings = stored_couplings
         self._h = h
         self._disc = disc
         self.opts = opts

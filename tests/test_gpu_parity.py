@@ -41,14 +41,17 @@ def _rel(a, b):
 def built(igb, po):
     cache = {}
 
-    def get(kind, P, rep, L, m):
-        key = (kind, P, rep, L, m)
+    def get(kind, P, rep, L, m, stored=False):
+        key = (kind, P, rep, L, m, stored)
         if key not in cache:
             g = igb.make_sphere()
             d = igb.Discretization(g, _pde(igb, kind), P, rep, L)
-            h = igb.H2Matrix(d, igb.H2Options(m=m, eta=1.6))
-            od = po.Discretization(kind, P, rep, L, kappa=KAPPA[kind])
-            oh = po.H2Matrix(od, m=m, eta=1.6)
+            h = igb.H2Matrix(d, igb.H2Options(m=m, eta=1.6), stored_couplings=stored)
+            okey = (kind, P, rep, L, m)
+            if okey not in cache:
+                od = po.Discretization(kind, P, rep, L, kappa=KAPPA[kind])
+                cache[okey] = (od, po.H2Matrix(od, m=m, eta=1.6))
+            od, oh = cache[okey]
             cache[key] = (d, h, od, oh)
         return cache[key]
     return get
@@ -71,9 +74,10 @@ def test_near_blocks(built, case):
     assert err.max() < TOL, f"worst block {err.argmax()} rel {err.max():.3e}"
 
 
+@pytest.mark.parametrize("stored", [False, True], ids=["fused", "stored"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
-def test_couplings_moments_images(built, case):
-    d, h, od, oh = built(*case)
+def test_couplings_moments_images(built, case, stored):
+    d, h, od, oh = built(*case, stored=stored)
     assert _rel(h.images(), oh.images()) < TOL
     assert _rel(h.moments(), oh.moments().real) < TOL
     n = min(h.far_count, 4000)
@@ -81,9 +85,10 @@ def test_couplings_moments_images(built, case):
         assert _rel(h.couplings(0, n), oh.couplings(0, n)) < TOL
 
 
+@pytest.mark.parametrize("stored", [False, True], ids=["fused", "stored"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
-def test_matvec(built, case):
-    d, h, od, oh = built(*case)
+def test_matvec(built, case, stored):
+    d, h, od, oh = built(*case, stored=stored)
     rng = np.random.default_rng(20261019)
     x = rng.uniform(-1, 1, d.dof_count())
     if h.dtype == np.complex128:
