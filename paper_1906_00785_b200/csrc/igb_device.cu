@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -970,12 +971,11 @@ __global__ void __launch_bounds__(256) k_far_fused(int n_targets, const int* __r
 // Branch-free FP64 reciprocal square root for normal positive inputs:
 // MUFU.RSQ64H seed (rsqrt.approx.ftz.f64, rel. err < 2^-22) + 2 Newton steps.
 __device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  // one cubic (Householder) step: y = y0 (1 + e/2 + 3e^2/8), e = 1 - x y0^2
+  const double e = fma(-x * y0, y0, 1.0);
+  return fma(y0 * e, fma(0.375, e, 0.5), y0);
 }
 
 template <int M>
@@ -992,8 +992,8 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
 // gives down[t] += K up[s] (accumulated in registers) and K^T up[t], written to
 // the slot of the transposed pair (s, t) and summed by k_far_lower in fixed
 // order.  Lane (bi, bj) owns RN target rows x CN source columns.
-template <int M>
-__global__ void __launch_bounds__(256) k_far_sym(int n_targets, const int* __restrict__ targets,
+template <int M, bool PF, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int* __restrict__ targets,
                                                  const int* __restrict__ upper_start, const int* __restrict__ far_rs,
                                                  const int* __restrict__ far_b, const int* __restrict__ trans,
                                                  const double* __restrict__ img, const double* __restrict__ up,
@@ -1019,20 +1019,35 @@ __global__ void __launch_bounds__(256) k_far_sym(int n_targets, const int* __res
     acc[i] = 0.0;
   }
   const int q0 = upper_start[t], q1 = far_rs[t + 1];
-  for (int q = q0; q < q1; ++q) {
+  // software pipeline: the next source cluster's images/moments are loaded
+  // while the current one is evaluated
+  double nsx[CN][3], nxs[CN];
+  auto load = [&](int q) {
     const int s = far_b[q];
-    double sx[CN][3], xs[CN], ps[CN];
 #pragma unroll
     for (int j = 0; j < CN; ++j) {
       const int mu = bj + BC * j;
       const bool ok = act && mu < MM;
       const double* p = img + (static_cast<size_t>(s) * MM + (ok ? mu : 0)) * 3;
-      sx[j][0] = __ldg(p);
-      sx[j][1] = __ldg(p + 1);
-      sx[j][2] = __ldg(p + 2);
-      xs[j] = ok ? __ldg(up + static_cast<size_t>(s) * MM + mu) : 0.0;
+      nsx[j][0] = __ldg(p);
+      nsx[j][1] = __ldg(p + 1);
+      nsx[j][2] = __ldg(p + 2);
+      nxs[j] = ok ? __ldg(up + static_cast<size_t>(s) * MM + mu) : 0.0;
+    }
+  };
+  if (PF && q0 < q1) load(q0);
+  for (int q = q0; q < q1; ++q) {
+    double sx[CN][3], xs[CN], ps[CN];
+    if (!PF) load(q);
+#pragma unroll
+    for (int j = 0; j < CN; ++j) {
+      sx[j][0] = nsx[j][0];
+      sx[j][1] = nsx[j][1];
+      sx[j][2] = nsx[j][2];
+      xs[j] = nxs[j];
       ps[j] = 0.0;
     }
+    if (PF && q + 1 < q1) load(q + 1);
 #pragma unroll
     for (int i = 0; i < RN; ++i)
 #pragma unroll
@@ -1121,13 +1136,12 @@ __global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, i
   Y[nu] = Y[nu] + acc;
 }
 
-// near rows + leaf backward transform per element (h2.cpp:349-376); one warp
+// near-field rows per test element (h2.cpp:349-357); one warp per element,
+// streaming its contiguous row [la][k][lb]
 template <class S, int NL>
-__global__ void __launch_bounds__(256) k_near_leaf(int ne, const int* __restrict__ near_rs,
+__global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict__ near_rs,
                                                    const int* __restrict__ near_b, const S* __restrict__ blk,
-                                                   const S* __restrict__ coef, int rows, int epp, int npp,
-                                                   int leaf_off, const double* __restrict__ mom,
-                                                   const S* __restrict__ down, S* __restrict__ loc) {
+                                                   const S* __restrict__ coef, S* __restrict__ rows_out) {
   const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (e >= ne) return;
@@ -1137,27 +1151,50 @@ __global__ void __launch_bounds__(256) k_near_leaf(int ne, const int* __restrict
   S acc[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) acc[l] = zero<S>();
-  for (int j = lane; j < len; j += 32) {
+  constexpr int U = (NL <= 9) ? 4 : 2;
+  int j = lane;
+  for (; j + 32 * (U - 1) < len; j += 32 * U) {
+    S xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int jj = j + 32 * u, k = jj / NL, lb = jj - k * NL;
+      xv[u] = coef[static_cast<size_t>(near_b[rs + k]) * NL + lb];
+    }
+#pragma unroll
+    for (int la = 0; la < NL; ++la)
+#pragma unroll
+      for (int u = 0; u < U; ++u) fmac(acc[la], ldg_s(base + static_cast<size_t>(la) * len + j + 32 * u), xv[u]);
+  }
+  for (; j < len; j += 32) {
     const int k = j / NL, lb = j - k * NL;
     const S xv = coef[static_cast<size_t>(near_b[rs + k]) * NL + lb];
 #pragma unroll
-    for (int la = 0; la < NL; ++la) fmac(acc[la], base[static_cast<size_t>(la) * len + j], xv);
+    for (int la = 0; la < NL; ++la) fmac(acc[la], ldg_s(base + static_cast<size_t>(la) * len + j), xv);
   }
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const S a = warp_sum(acc[l]);
+    if (lane == 0) rows_out[static_cast<size_t>(e) * NL + l] = a;
+  }
+}
+
+// leaf backward transform moments^T down + near rows (h2.cpp:359-371); one warp per element
+template <class S, int NL>
+__global__ void __launch_bounds__(256) k_leaf_down(int ne, int rows, int epp, int npp, int leaf_off,
+                                                   const double* __restrict__ mom, const S* __restrict__ down,
+                                                   const S* __restrict__ near_rows, S* __restrict__ loc) {
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= ne) return;
   const int leaf = (e / epp) * npp + leaf_off + (e % epp);
   const S* dn = down + static_cast<size_t>(leaf) * rows;
-  S lf[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
     S s = zero<S>();
     const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
     for (int r = lane; r < rows; r += 32) fmac(s, dn[r], mc[r]);
-    lf[l] = s;
-  }
-#pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    const S a = warp_sum(acc[l]);
-    const S b = warp_sum(lf[l]);
-    if (lane == 0) loc[static_cast<size_t>(e) * NL + l] = a + b;
+    const S b = warp_sum(s);
+    if (lane == 0) loc[static_cast<size_t>(e) * NL + l] = near_rows[static_cast<size_t>(e) * NL + l] + b;
   }
 }
 
@@ -1261,6 +1298,9 @@ H2Device::~H2Device() {
   for (void* p : allocs_) cudaFree(p);
   if (h_x_pinned_) cudaFreeHost(h_x_pinned_);
   if (h_y_pinned_) cudaFreeHost(h_y_pinned_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (side_) cudaStreamDestroy(side_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -1417,6 +1457,10 @@ void H2Device::assemble_impl() {
   d_up_ = dalloc<double>(nn * rows * sw);
   d_down_ = dalloc<double>(nn * rows * sw);
   d_loc_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
+  d_nrows_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
+  IGB_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  IGB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  IGB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1614,6 +1658,18 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
   k_coef<S><<<grid_for(nloc, 256), 256, 0, s>>>(nloc, x, d_l2g_, d_lsign_, coef);
   ++launches;
   mark(1);
+  // near-field rows (HBM-bound) run on a forked stream, overlapping the
+  // latency-bound upward/downward passes and the FP64-bound far field
+  S* nrows = reinterpret_cast<S*>(d_nrows_);
+  const bool fork = (pev == nullptr);
+  if (fork) {
+    IGB_CUDA(cudaEventRecord(ev_fork_, s));
+    IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+    k_near_rows<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, side_>>>(
+        ne, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
+    ++launches;
+    IGB_CUDA(cudaEventRecord(ev_join_, side_));
+  }
   k_leaf_up<S><<<grid_for(static_cast<long long>(ne) * rows, 256), 256, 0, s>>>(ne, NL, rows, epp, npp,
                                                                                  P.level_offset[L], d_mom_, coef, up);
   ++launches;
@@ -1654,13 +1710,17 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
       const unsigned gsym = grid_for(static_cast<long long>(n_sym_targets_) * 32, 256);
       double* dn = reinterpret_cast<double*>(down);
       const double* upd = reinterpret_cast<const double*>(up);
-      switch (m) {
-        case 2: k_far_sym<2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-        case 3: k_far_sym<3><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-        case 4: k_far_sym<4><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-        case 5: k_far_sym<5><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-        default: k_far_sym<6><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+#define IGB_FS(MM_, MB_)                                                                                        \
+  k_far_sym<MM_, false, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,        \
+                                                 d_far_b_, d_trans_, d_img_, upd, dn, d_slot_)
+      switch (m) {  // occupancy chosen so no variant spills (ptxas -warn-spills)
+        case 2: IGB_FS(2, 3); break;
+        case 3: IGB_FS(3, 3); break;
+        case 4: IGB_FS(4, 3); break;
+        case 5: IGB_FS(5, 2); break;
+        default: IGB_FS(6, 2); break;
       }
+#undef IGB_FS
       ++launches;
       k_far_lower<<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(P.n_nodes, mm, d_far_rs_, d_upper_start_, d_slot_, dn);
     } else {
@@ -1691,9 +1751,15 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
     ++launches;
   }
   mark(6);
-  k_near_leaf<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, s>>>(
-      ne, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, rows, epp, npp, P.level_offset[L], d_mom_,
-      down, loc);
+  if (fork) {
+    IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+  } else {
+    k_near_rows<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, s>>>(
+        ne, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
+    ++launches;
+  }
+  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, s>>>(
+      ne, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
   ++launches;
   mark(7);
   k_scatter<S><<<grid_for(d.dof_count(), 256), 256, 0, s>>>(d.dof_count(), d_dof_start_, d_dof_inc_, d_lsign_, loc, y);

@@ -115,6 +115,9 @@ class H2Device {
   double *dx_ = nullptr, *dy_ = nullptr, *d_coef_ = nullptr, *d_up_ = nullptr, *d_down_ = nullptr,
          *d_loc_ = nullptr;
   double *h_x_pinned_ = nullptr, *h_y_pinned_ = nullptr;
+  double* d_nrows_ = nullptr;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   int apply_launches_ = 0;
   int assembly_kernels_ = 0, assembly_launches_count_ = 0;
