@@ -104,6 +104,17 @@ int igb_h2_create(const igb_discretization* d, const igb_h2_opts* opts, int devi
  * on the fly inside the matvec (same values, no coupling storage) */
 enum { IGB_H2_STORED_COUPLINGS = 2 };
 int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, igb_h2** out);
+/* ---- multi-GPU row-cluster partition ----
+ * rank `rank` of `world` assembles and applies the block rows of its level-1
+ * clusters.  Matvec: igb_h2_dist_phase1(x -> send), all-gather `send` of
+ * every rank into `recv` (rank-major, igb_h2_dist_send_count scalars each),
+ * igb_h2_dist_phase2(recv -> y_partial), all-reduce(sum) y_partial.  All
+ * pointers are device pointers; work is enqueued on `stream`. */
+int igb_h2_create_dist(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, int world,
+                       int rank, igb_h2** out);
+int igb_h2_dist_send_count(const igb_h2* h, size_t* scalars);
+int igb_h2_dist_phase1(igb_h2* h, const double* x, double* send, void* stream);
+int igb_h2_dist_phase2(igb_h2* h, const double* recv, double* y_partial, void* stream);
 /* rows()/cols()  h2.hpp:62-63 */
 int igb_h2_dim(const igb_h2* h, int* rows);
 /* apply(x) / operator*  h2.hpp:64-69, h2.cpp:254-378: host buffers of rows()
@@ -181,6 +192,9 @@ int igb_plan_class_counts(const igb_plan* p, long long counts[4]);
  * far pairs whose test element / target node lies in them */
 int igb_plan_partition(const igb_plan* p, int world, int rank, int* c0, int* c1, int* n_elements,
                        long long* n_near, long long* n_far);
+/* ownership masks of that rank: element_owned[ne], node_owned[n_nodes]
+ * (roots are owned by every rank) */
+int igb_plan_owned(const igb_plan* p, int world, int rank, unsigned char* element_owned, unsigned char* node_owned);
 void igb_plan_destroy(igb_plan* p);
 
 /* eta-admissibility of two boxes (min xyz, max xyz), h2.cpp:92-97 */

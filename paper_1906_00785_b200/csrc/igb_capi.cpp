@@ -205,6 +205,37 @@ int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int d
     *out = new igb_h2{std::make_unique<igb::H2Device>(d->d, o.m, o.eta, o.far_order, o.sing_order, device, flags)};
   });
 }
+int igb_h2_create_dist(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, int world,
+                       int rank, igb_h2** out) {
+  return guard([&] {
+    need(d, "discretization");
+    need(out, "out");
+    igb_h2_opts o = opts ? *opts : igb_h2_opts{8, 1.6, 0, 0};
+    *out = new igb_h2{
+        std::make_unique<igb::H2Device>(d->d, o.m, o.eta, o.far_order, o.sing_order, device, flags, world, rank)};
+  });
+}
+int igb_h2_dist_send_count(const igb_h2* h, size_t* scalars) {
+  return guard([&] {
+    need(h, "h2");
+    need(scalars, "scalars");
+    *scalars = h->dev->send_count();
+  });
+}
+int igb_h2_dist_phase1(igb_h2* h, const double* x, double* send, void* stream) {
+  return guard([&] {
+    need(h, "h2");
+    need(x, "x");
+    h->dev->dist_phase1(x, send, static_cast<cudaStream_t>(stream));
+  });
+}
+int igb_h2_dist_phase2(igb_h2* h, const double* recv, double* y, void* stream) {
+  return guard([&] {
+    need(h, "h2");
+    need(y, "y");
+    h->dev->dist_phase2(recv, y, static_cast<cudaStream_t>(stream));
+  });
+}
 int igb_h2_dim(const igb_h2* h, int* rows) {
   return guard([&] {
     need(h, "h2");
@@ -470,6 +501,15 @@ int igb_plan_partition(const igb_plan* p, int world, int rank, int* c0, int* c1,
     if (n_elements) *n_elements = static_cast<int>(r.elements.size());
     if (n_near) *n_near = r.near_count;
     if (n_far) *n_far = r.far_count;
+  });
+}
+int igb_plan_owned(const igb_plan* p, int world, int rank, unsigned char* element_owned, unsigned char* node_owned) {
+  return guard([&] {
+    need(p, "plan");
+    const auto lp = igb::build_local_plan(*p->d, p->plan, world, rank);
+    if (element_owned)
+      for (size_t e = 0; e < lp.el_local.size(); ++e) element_owned[e] = lp.el_local[e] >= 0 ? 1 : 0;
+    if (node_owned) std::copy(lp.node_owned.begin(), lp.node_owned.end(), node_owned);
   });
 }
 void igb_plan_destroy(igb_plan* p) { delete p; }

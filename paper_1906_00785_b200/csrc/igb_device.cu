@@ -450,15 +450,15 @@ __global__ void __launch_bounds__(256) k_couplings(long long n_pairs, int mm, co
 template <class KT>
 __global__ void __launch_bounds__(128) k_regular(const int* __restrict__ slots, const int* __restrict__ near_a,
                                                  const int* __restrict__ near_b, const int* __restrict__ near_rs,
-                                                 int nq, const double* __restrict__ cpts,
-                                                 const double* __restrict__ cval, KParams kp,
-                                                 double* __restrict__ near) {
+                                                 const int* __restrict__ near_ea, int nq,
+                                                 const double* __restrict__ cpts, const double* __restrict__ cval,
+                                                 KParams kp, double* __restrict__ near) {
   using S = typename KT::S;
   constexpr int NL = KT::NL, NC = KT::NC;
   extern __shared__ __align__(16) double sm[];
   S* KB = reinterpret_cast<S*>(sm);  // [NC][nq][NL]
   const int q = slots[blockIdx.x];
-  const int ea = near_a[q], eb = near_b[q];
+  const int ea = near_ea[q], eb = near_b[q];
   const double* pa = cpts + static_cast<size_t>(ea) * nq * 3;
   const double* pb = cpts + static_cast<size_t>(eb) * nq * 3;
   for (int it = threadIdx.x; it < nq * NC; it += blockDim.x) {
@@ -724,8 +724,8 @@ __global__ void __launch_bounds__(128) k_singular(GeoArgs g, SingArgs A) {
     S v = zero<S>();
     for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + o];
     const int la = o / NL, lb = o % NL;
-    out[near_off(A.near_a, A.near_rs, qab, la, lb, NL)] = v;
-    if (qba != qab) out[near_off(A.near_a, A.near_rs, qba, lb, la, NL)] = v;
+    if (qab >= 0) out[near_off(A.near_a, A.near_rs, qab, la, lb, NL)] = v;
+    if (qba >= 0 && qba != qab) out[near_off(A.near_a, A.near_rs, qba, lb, la, NL)] = v;
   }
 }
 
@@ -739,28 +739,49 @@ __global__ void k_coef(int n, const S* __restrict__ x, const int* __restrict__ l
 __device__ __forceinline__ double operator_mul(double a, double b) { return a * b; }
 
 template <class S>
-__global__ void k_leaf_up(int ne, int nl, int rows, int epp, int npp, int leaf_off, const double* __restrict__ mom,
-                          const S* __restrict__ coef, S* __restrict__ up) {  // h2.cpp:281-290
+__global__ void k_leaf_up(int n_el, const int* __restrict__ el, int nl, int rows, int epp, int npp, int leaf_off,
+                          const double* __restrict__ mom, const S* __restrict__ coef,
+                          S* __restrict__ up) {  // h2.cpp:281-290, owned leaves
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= static_cast<long long>(ne) * rows) return;
-  const int e = static_cast<int>(idx / rows), r = static_cast<int>(idx % rows);
+  if (idx >= static_cast<long long>(n_el) * rows) return;
+  const int e = el[idx / rows], r = static_cast<int>(idx % rows);
   S acc = zero<S>();
   for (int l = 0; l < nl; ++l) fmac(acc, coef[static_cast<size_t>(e) * nl + l], mom[(static_cast<size_t>(e) * nl + l) * rows + r]);
   const int leaf = (e / epp) * npp + leaf_off + (e % epp);
   up[static_cast<size_t>(leaf) * rows + r] = acc;
 }
 
-// parent(i,j) = sum_k tu_k X_k tv_k^T  (h2.cpp:291-310)
+// node of a level-l tree in level-1 cluster c (l >= 1), local index sc
+__device__ __forceinline__ void cluster_node(int c, int level, int sc, int& p, int& sx, int& sy) {
+  const int half = 1 << (level - 1);
+  const int k1 = c & 3;
+  p = c >> 2;
+  sx = (k1 & 1) * half + sc % half;
+  sy = (k1 >> 1) * half + sc / half;
+}
+
+// parent(i,j) = sum_k tu_k X_k tv_k^T  (h2.cpp:291-310); level 0: all roots,
+// level >= 1: the nodes of level-1 clusters [c0, c1)
 template <class S>
 __global__ void k_up_level(int np, int level, int npp, int off_l, int off_c, int m, int nch,
-                           const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ up) {
-  const int mm = m * m, rows = nch * mm, nside = 1 << level, per = nside * nside;
+                           const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ up, int c0,
+                           int c1) {
+  const int mm = m * m, rows = nch * mm, nside = 1 << level;
+  const int per = level == 0 ? 1 : (1 << (2 * (level - 1)));
+  const int ncl = level == 0 ? np : (c1 - c0);
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= static_cast<long long>(np) * per * rows) return;
+  if (idx >= static_cast<long long>(ncl) * per * rows) return;
   const int r = static_cast<int>(idx % rows);
   const long long nidx = idx / rows;
-  const int p = static_cast<int>(nidx / per), s = static_cast<int>(nidx % per);
-  const int sx = s % nside, sy = s / nside, c = r / mm, nu = r % mm, i = nu % m, j = nu / m;
+  const int ci = static_cast<int>(nidx / per), sc = static_cast<int>(nidx % per);
+  int p, sx, sy;
+  if (level == 0) {
+    p = ci;
+    sx = sy = 0;
+  } else {
+    cluster_node(c0 + ci, level, sc, p, sx, sy);
+  }
+  const int c = r / mm, nu = r % mm, i = nu % m, j = nu / m;
   const int cside = nside * 2;
   S acc = zero<S>();
   for (int k = 0; k < 4; ++k) {
@@ -774,7 +795,7 @@ __global__ void k_up_level(int np, int level, int npp, int off_l, int off_c, int
       fmac(acc, t, tv[j + m * b]);
     }
   }
-  up[static_cast<size_t>(p * npp + off_l + s) * rows + r] = acc;
+  up[static_cast<size_t>(p * npp + off_l + sx + nside * sy) * rows + r] = acc;
 }
 
 // down[t] = sum_q w_c K_q up[tb_q]  (h2.cpp:312-326); one warp per target
@@ -997,7 +1018,8 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
                                                  const int* __restrict__ upper_start, const int* __restrict__ far_rs,
                                                  const int* __restrict__ far_b, const int* __restrict__ trans,
                                                  const double* __restrict__ img, const double* __restrict__ up,
-                                                 double* __restrict__ down, double* __restrict__ slot) {
+                                                 double* __restrict__ down, double* __restrict__ slot,
+                                                 const unsigned char* __restrict__ owned, int full_row) {
   using T = SymTile<M>;
   constexpr int MM = T::MM, BR = T::BR, BC = T::BC, RN = T::RN, CN = T::CN;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1018,7 +1040,10 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
     xt[i] = ok ? up[static_cast<size_t>(t) * MM + nu] : 0.0;
     acc[i] = 0.0;
   }
-  const int q0 = upper_start[t], q1 = far_rs[t + 1];
+  // pairs (t, s): s > t and s owned -> symmetric (t's row + slot of (s, t));
+  // s not owned (other rank's block rows) -> one-sided; s < t owned -> skip
+  // (evaluated by s's warp).  Single GPU: every s owned, only s > t visited.
+  const int q0 = full_row ? far_rs[t] : upper_start[t], q1 = far_rs[t + 1];
   // software pipeline: the next source cluster's images/moments are loaded
   // while the current one is evaluated
   double nsx[CN][3], nxs[CN];
@@ -1037,6 +1062,9 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
   };
   if (PF && q0 < q1) load(q0);
   for (int q = q0; q < q1; ++q) {
+    const int sq = far_b[q];
+    const bool own_s = owned[sq] != 0;
+    if (own_s && sq < t) continue;  // warp-uniform
     double sx[CN][3], xs[CN], ps[CN];
     if (!PF) load(q);
 #pragma unroll
@@ -1057,6 +1085,7 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
         acc[i] = fma(gk, xs[j], acc[i]);
         ps[j] = fma(gk, xt[i], ps[j]);
       }
+    if (!own_s) continue;  // one-sided pair: no transposed product
     // K^T up[t] for the CN columns: reduce over the BR lanes of the column
 #pragma unroll
     for (int j = 0; j < CN; ++j) {
@@ -1100,28 +1129,34 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
 // in ascending t (fixed order)
 __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs, const int* __restrict__ upper_start,
+                            const int* __restrict__ far_b, const unsigned char* __restrict__ owned,
                             const double* __restrict__ slot, double* __restrict__ down) {
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n_nodes) * mm) return;
   const int s = static_cast<int>(idx / mm), nu = static_cast<int>(idx % mm);
   const int q0 = far_rs[s], q1 = upper_start[s];
-  if (q0 == q1) return;
+  if (q0 == q1 || !owned[s]) return;
   double acc = down[idx];
-  for (int q = q0; q < q1; ++q) acc += slot[static_cast<size_t>(q) * mm + nu];
+  for (int q = q0; q < q1; ++q)
+    if (owned[far_b[q]]) acc += slot[static_cast<size_t>(q) * mm + nu];
   down[idx] = acc;
 }
 
-// child(i,j) += tu^T X tv  (h2.cpp:328-347)
+// child(i,j) += tu^T X tv  (h2.cpp:328-347): children at level+1 >= 1 in
+// level-1 clusters [c0, c1)
 template <class S>
 __global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, int m, int nch,
-                             const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ down) {
-  const int mm = m * m, rows = nch * mm, cside = 2 << level, per = cside * cside;
+                             const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ down,
+                             int c0, int c1) {
+  (void)np;
+  const int mm = m * m, rows = nch * mm, cside = 2 << level, per = 1 << (2 * level);
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= static_cast<long long>(np) * per * rows) return;
+  if (idx >= static_cast<long long>(c1 - c0) * per * rows) return;
   const int r = static_cast<int>(idx % rows);
   const long long nidx = idx / rows;
-  const int p = static_cast<int>(nidx / per), s = static_cast<int>(nidx % per);
-  const int sx = s % cside, sy = s / cside, c = r / mm, nu = r % mm, i = nu % m, j = nu / m;
+  int p, sx, sy;
+  cluster_node(c0 + static_cast<int>(nidx / per), level + 1, static_cast<int>(nidx % per), p, sx, sy);
+  const int c = r / mm, nu = r % mm, i = nu % m, j = nu / m;
   const int parent = p * npp + off_p + (sx / 2) + (cside / 2) * (sy / 2);
   const double* tu = (sx & 1) ? tr : tl;
   const double* tv = (sy & 1) ? tr : tl;
@@ -1132,8 +1167,23 @@ __global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, i
     for (int a = 0; a < m; ++a) fmac(t, X[a + m * b], tu[a + m * i]);
     fmac(acc, t, tv[b + m * j]);
   }
-  S* Y = down + static_cast<size_t>(p * npp + off_c + s) * rows + c * mm;
+  S* Y = down + static_cast<size_t>(p * npp + off_c + sx + cside * sy) * rows + c * mm;
   Y[nu] = Y[nu] + acc;
+}
+
+// all-gather payload of the up moments (owned nodes, levels >= 1)
+template <class S>
+__global__ void k_pack(int n, const int* __restrict__ nodes, int rows, const S* __restrict__ up, S* __restrict__ send) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n) * rows) return;
+  send[idx] = up[static_cast<size_t>(nodes[idx / rows]) * rows + idx % rows];
+}
+template <class S>
+__global__ void k_unpack(int n, const int* __restrict__ nodes, int rows, const S* __restrict__ recv, S* __restrict__ up) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n) * rows) return;
+  const int node = nodes[idx / rows];
+  if (node >= 0) up[static_cast<size_t>(node) * rows + idx % rows] = recv[idx];
 }
 
 // near-field rows per test element (h2.cpp:349-357); one warp per element,
@@ -1180,12 +1230,14 @@ __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict
 
 // leaf backward transform moments^T down + near rows (h2.cpp:359-371); one warp per element
 template <class S, int NL>
-__global__ void __launch_bounds__(256) k_leaf_down(int ne, int rows, int epp, int npp, int leaf_off,
-                                                   const double* __restrict__ mom, const S* __restrict__ down,
-                                                   const S* __restrict__ near_rows, S* __restrict__ loc) {
-  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restrict__ el, int rows, int epp, int npp,
+                                                   int leaf_off, const double* __restrict__ mom,
+                                                   const S* __restrict__ down, const S* __restrict__ near_rows,
+                                                   S* __restrict__ loc) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (e >= ne) return;
+  if (i >= n_el) return;
+  const int e = el[i];
   const int leaf = (e / epp) * npp + leaf_off + (e % epp);
   const S* dn = down + static_cast<size_t>(leaf) * rows;
 #pragma unroll
@@ -1194,7 +1246,7 @@ __global__ void __launch_bounds__(256) k_leaf_down(int ne, int rows, int epp, in
     const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
     for (int r = lane; r < rows; r += 32) fmac(s, dn[r], mc[r]);
     const S b = warp_sum(s);
-    if (lane == 0) loc[static_cast<size_t>(e) * NL + l] = near_rows[static_cast<size_t>(e) * NL + l] + b;
+    if (lane == 0) loc[static_cast<size_t>(i) * NL + l] = near_rows[static_cast<size_t>(i) * NL + l] + b;
   }
 }
 
@@ -1241,8 +1293,10 @@ T* H2Device::upload(const std::vector<T>& v) {
 static unsigned grid_for(long long n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
 H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, int far_order, int sing_order,
-                   int device, int flags)
+                   int device, int flags, int world, int rank)
     : disc_(std::move(d)), device_(device), flags_(flags) {
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("H2Matrix: bad rank/world");
+  if (world > 1 && (flags & 2)) throw std::invalid_argument("H2Matrix: stored couplings are single-GPU only");
   const auto t_wall0 = std::chrono::steady_clock::now();
   int ndev = 0;
   IGB_CUDA(cudaGetDeviceCount(&ndev));
@@ -1251,6 +1305,7 @@ H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, i
   IGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   const auto t0 = std::chrono::steady_clock::now();
   plan_ = build_plan(*disc_, m, eta, far_order, sing_order);
+  lp_ = build_local_plan(*disc_, plan_, world, rank);
   times_.plan_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   nch_ = disc_->is_vector() ? 4 : 1;
   const int kind = disc_->kind();
@@ -1361,24 +1416,40 @@ void H2Device::assemble_impl() {
   d_tab_b_ = upload(d.is_vector() ? d.tab_q() : std::vector<double>(1, 0.0));
   d_l2g_ = upload(d.l2g());
   d_lsign_ = upload(d.lsign());
-  d_near_a_ = upload(P.near_a);
-  d_near_b_ = upload(P.near_b);
-  d_near_rs_ = upload(P.near_row_start);
+  const LocalPlan& Lp = lp_;
+  d_near_a_ = upload(Lp.near_row);  // local row of each local near slot
+  d_near_b_ = upload(Lp.near_eb);
+  d_near_ea_ = upload(Lp.near_ea);
+  d_near_rs_ = upload(Lp.near_rs);
+  d_el_ = upload(Lp.el);
+  d_owned_ = upload(Lp.node_owned);
+  {
+    std::vector<double> sg(Lp.el.size() * static_cast<size_t>(d.local_count()));
+    for (size_t i = 0; i < Lp.el.size(); ++i)
+      for (int l = 0; l < d.local_count(); ++l)
+        sg[i * d.local_count() + l] = d.lsign()[static_cast<size_t>(Lp.el[i]) * d.local_count() + l];
+    d_loc_sign_ = upload(sg);
+  }
+  if (Lp.world > 1) {
+    d_pack_nodes_ = upload(Lp.pack_nodes);
+    std::vector<int> un(static_cast<size_t>(Lp.world) * Lp.pack_max, -1);
+    for (int r = 0; r < Lp.world; ++r)
+      for (size_t i = 0; i < Lp.rank_pack_nodes[r].size(); ++i) un[static_cast<size_t>(r) * Lp.pack_max + i] = Lp.rank_pack_nodes[r][i];
+    d_unpack_nodes_ = upload(un);
+  }
   d_far_a_ = upload(P.far_a);
   d_far_b_ = upload(P.far_b);
   d_far_rs_ = upload(P.far_row_start);
   {
-    std::vector<int> targets;
-    for (int t = 0; t < P.n_nodes; ++t)
-      if (P.far_row_start[t + 1] > P.far_row_start[t]) targets.push_back(t);
+    const std::vector<int>& targets = Lp.far_targets;
     n_far_targets_ = static_cast<int>(targets.size());
     d_far_targets_ = upload(targets);
     // symmetric fused far field (Laplace, m <= 6): upper pairs + transposes
     sym_far_ = !stored_couplings() && d.kind() == kLaplace && m >= 2 && m <= 6;
     if (sym_far_) {
       std::vector<int> sym_targets;
-      for (int t = 0; t < P.n_nodes; ++t)
-        if (P.far_upper_start[t] < P.far_row_start[t + 1]) sym_targets.push_back(t);
+      for (int t : Lp.far_targets)
+        if (Lp.world > 1 || P.far_upper_start[t] < P.far_row_start[t + 1]) sym_targets.push_back(t);
       n_sym_targets_ = static_cast<int>(sym_targets.size());
       d_sym_targets_ = upload(sym_targets);
       d_upper_start_ = upload(P.far_upper_start);
@@ -1386,8 +1457,8 @@ void H2Device::assemble_impl() {
       d_slot_ = dalloc<double>(P.far_a.size() * static_cast<size_t>(mm));
     }
   }
-  d_dof_start_ = upload(P.dof_start);
-  d_dof_inc_ = upload(P.dof_inc);
+  d_dof_start_ = upload(Lp.dof_start);
+  d_dof_inc_ = upload(Lp.dof_inc);
   d_tl_ = upload(P.tl);
   d_tr_ = upload(P.tr);
   int* d_np = upload(P.node_patch);
@@ -1417,7 +1488,7 @@ void H2Device::assemble_impl() {
   }
   as_.lag = upload(lag);
   for (int c = 1; c <= 3; ++c) {
-    const auto& L = P.sing[c];
+    const auto& L = Lp.sing[c];
     as_.sing[c][0] = upload(L.ea);
     as_.sing[c][1] = upload(L.eb);
     as_.sing[c][2] = upload(L.slot_ab);
@@ -1425,13 +1496,13 @@ void H2Device::assemble_impl() {
     as_.singm[c][0] = upload(L.map_a);
     as_.singm[c][1] = upload(L.map_b);
   }
-  as_.reg = upload(P.reg_slot);
+  as_.reg = upload(Lp.reg_slot);
   as_.kp[0] = kp.kr;
   as_.kp[1] = kp.ki;
   as_.kp[2] = kp.dwx;
   as_.kp[3] = kp.dwy;
 
-  const long long nnear = static_cast<long long>(P.near_a.size());
+  const long long nnear = static_cast<long long>(Lp.near_row.size());
   const long long nfarp = static_cast<long long>(P.far_a.size());
   const int nf = P.nfar, nq = nf * nf;
   d_near_ = dalloc<double>(static_cast<size_t>(nnear) * NL * NL * sw);
@@ -1454,10 +1525,14 @@ void H2Device::assemble_impl() {
   dx_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
   dy_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
   d_coef_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
+  if (Lp.world > 1) {
+    d_send_ = dalloc<double>(static_cast<size_t>(Lp.pack_max) * rows * sw);
+    d_recv_ = dalloc<double>(static_cast<size_t>(Lp.pack_max) * Lp.world * rows * sw);
+  }
   d_up_ = dalloc<double>(nn * rows * sw);
   d_down_ = dalloc<double>(nn * rows * sw);
-  d_loc_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
-  d_nrows_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
+  d_loc_ = dalloc<double>(Lp.el.size() * NL * sw);
+  d_nrows_ = dalloc<double>(Lp.el.size() * NL * sw);
   IGB_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
   IGB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   IGB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
@@ -1541,12 +1616,12 @@ void H2Device::run_assembly() {
   }
   IGB_CUDA(cudaEventRecord(ev[4], stream_));
   // ---- K4 regular near
-  if (!P.reg_slot.empty()) {
+  if (!lp_.reg_slot.empty()) {
     const size_t smem = static_cast<size_t>(NC) * nq * NL * 8 * sw;
     IGB_CUDA(cudaFuncSetAttribute(k_regular<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     if (smem > 200 * 1024) throw std::invalid_argument("B200 H2: far quadrature order too large");
-    k_regular<KT><<<static_cast<unsigned>(P.reg_slot.size()), 128, smem, stream_>>>(
-        d_reg, d_near_a_, d_near_b_, d_near_rs_, nq, d_cpts_, d_cval_, kp, d_near_);
+    k_regular<KT><<<static_cast<unsigned>(lp_.reg_slot.size()), 128, smem, stream_>>>(
+        d_reg, d_near_a_, d_near_b_, d_near_rs_, d_near_ea_, nq, d_cpts_, d_cval_, kp, d_near_);
     ++launched;
     IGB_CUDA(cudaGetLastError());
   }
@@ -1558,7 +1633,7 @@ void H2Device::run_assembly() {
     if (P.nsing > 16) throw std::invalid_argument("B200 H2: singular order > 16 not supported (32-bit point index)");
     auto launch = [&](auto cls_tag, int c, int evi) {
       constexpr int CLS = decltype(cls_tag)::value;
-      const auto& L = P.sing[c];
+      const auto& L = lp_.sing[c];
       if (!L.ea.empty()) {
         SingArgs A;
         A.n_pairs = static_cast<int>(L.ea.size());
@@ -1635,21 +1710,22 @@ double H2Device::reassemble() {
   return times_.total_device;
 }
 
+// Matvec, phase 1 (h2.cpp:271-310): coefficient gather, near rows on the
+// forked side stream, leaf moments and upward transfer of the owned clusters,
+// and (multi-GPU) the all-gather payload.
 template <class KT>
-void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cudaEvent_t* pev) {
+void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, cudaEvent_t* pev, int& launches) {
   using S = typename KT::S;
   constexpr int NL = KT::NL;
   const Discretization& d = *disc_;
   const H2Plan& P = plan_;
+  const LocalPlan& Lp = lp_;
   const int ne = d.element_count(), m = P.m, mm = m * m, rows = nch_ * mm, L = P.depth;
   const int np = P.n_patches, npp = P.npp, epp = d.elements_per_patch();
+  const int nel = static_cast<int>(Lp.el.size());
   const S* x = reinterpret_cast<const S*>(xin);
-  S* y = reinterpret_cast<S*>(yout);
   S* coef = reinterpret_cast<S*>(d_coef_);
   S* up = reinterpret_cast<S*>(d_up_);
-  S* down = reinterpret_cast<S*>(d_down_);
-  S* loc = reinterpret_cast<S*>(d_loc_);
-  int launches = 0;
   auto mark = [&](int i) {
     if (pev) IGB_CUDA(cudaEventRecord(pev[i], s));
   };
@@ -1661,23 +1737,64 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
   // near-field rows (HBM-bound) run on a forked stream, overlapping the
   // latency-bound upward/downward passes and the FP64-bound far field
   S* nrows = reinterpret_cast<S*>(d_nrows_);
-  const bool fork = (pev == nullptr);
-  if (fork) {
+  if (pev == nullptr) {
     IGB_CUDA(cudaEventRecord(ev_fork_, s));
     IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-    k_near_rows<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, side_>>>(
-        ne, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
+    k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
+        nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
     ++launches;
     IGB_CUDA(cudaEventRecord(ev_join_, side_));
   }
-  k_leaf_up<S><<<grid_for(static_cast<long long>(ne) * rows, 256), 256, 0, s>>>(ne, NL, rows, epp, npp,
-                                                                                 P.level_offset[L], d_mom_, coef, up);
+  k_leaf_up<S><<<grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s>>>(
+      nel, d_el_, NL, rows, epp, npp, P.level_offset[L], d_mom_, coef, up);
   ++launches;
   mark(2);
-  for (int l = L - 1; l >= 0; --l) {
-    const long long tot = static_cast<long long>(np) * (1LL << (2 * l)) * rows;
+  for (int l = L - 1; l >= 1; --l) {
+    const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * (l - 1))) * rows;
     k_up_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
-                                                      d_tl_, d_tr_, up);
+                                                      d_tl_, d_tr_, up, Lp.c0, Lp.c1);
+    ++launches;
+  }
+  if (Lp.world > 1 && Lp.pack_nodes.size()) {
+    const long long tot = static_cast<long long>(Lp.pack_nodes.size()) * rows;
+    k_pack<S><<<grid_for(tot, 256), 256, 0, s>>>(static_cast<int>(Lp.pack_nodes.size()), d_pack_nodes_, rows, up,
+                                                  reinterpret_cast<S*>(send));
+    ++launches;
+  }
+}
+
+// Matvec, phase 2 (h2.cpp:291-376): (multi-GPU) unpack the gathered moments,
+// root transfer, far field of the owned targets, downward transfer, leaf
+// backward transform + near rows, deterministic DOF gather.
+template <class KT>
+void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, cudaEvent_t* pev, int& launches) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL;
+  const Discretization& d = *disc_;
+  const H2Plan& P = plan_;
+  const LocalPlan& Lp = lp_;
+  const int m = P.m, mm = m * m, rows = nch_ * mm, L = P.depth;
+  const int np = P.n_patches, npp = P.npp, epp = d.elements_per_patch();
+  const int nel = static_cast<int>(Lp.el.size());
+  S* y = reinterpret_cast<S*>(yout);
+  S* coef = reinterpret_cast<S*>(d_coef_);
+  S* up = reinterpret_cast<S*>(d_up_);
+  S* down = reinterpret_cast<S*>(d_down_);
+  S* loc = reinterpret_cast<S*>(d_loc_);
+  S* nrows = reinterpret_cast<S*>(d_nrows_);
+  auto mark = [&](int i) {
+    if (pev) IGB_CUDA(cudaEventRecord(pev[i], s));
+  };
+  if (Lp.world > 1) {
+    const long long tot = static_cast<long long>(Lp.world) * Lp.pack_max * rows;
+    k_unpack<S><<<grid_for(tot, 256), 256, 0, s>>>(Lp.world * Lp.pack_max, d_unpack_nodes_, rows,
+                                                    reinterpret_cast<const S*>(recv), up);
+    ++launches;
+  }
+  if (L >= 1) {  // roots (replicated on every rank)
+    const long long tot = static_cast<long long>(np) * rows;
+    k_up_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, 0, npp, P.level_offset[0], P.level_offset[1], m, nch_,
+                                                      d_tl_, d_tr_, up, 0, 0);
     ++launches;
   }
   mark(3);
@@ -1712,17 +1829,18 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
       const double* upd = reinterpret_cast<const double*>(up);
 #define IGB_FS(MM_, MB_)                                                                                        \
   k_far_sym<MM_, false, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,        \
-                                                 d_far_b_, d_trans_, d_img_, upd, dn, d_slot_)
+                                                 d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, \
+                                                 d_owned_, lp_.world > 1 ? 1 : 0)
       switch (m) {  // occupancy chosen so no variant spills (ptxas -warn-spills)
         case 2: IGB_FS(2, 3); break;
         case 3: IGB_FS(3, 3); break;
         case 4: IGB_FS(4, 3); break;
         case 5: IGB_FS(5, 2); break;
-        default: IGB_FS(6, 2); break;
+        default: IGB_FS(6, 1); break;
       }
 #undef IGB_FS
       ++launches;
-      k_far_lower<<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(P.n_nodes, mm, d_far_rs_, d_upper_start_, d_slot_, dn);
+      k_far_lower<<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn);
     } else {
       KParams kp;
       kp.kr = as_.kp[0];
@@ -1745,28 +1863,77 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
   }
   mark(5);
   for (int l = 0; l < L; ++l) {
-    const long long tot = static_cast<long long>(np) * (4LL << (2 * l)) * rows;
+    const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
     k_down_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, l, npp, P.level_offset[l], P.level_offset[l + 1], m,
-                                                        nch_, d_tl_, d_tr_, down);
+                                                        nch_, d_tl_, d_tr_, down, Lp.c0, Lp.c1);
     ++launches;
   }
   mark(6);
-  if (fork) {
+  if (pev == nullptr) {
     IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
   } else {
-    k_near_rows<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, s>>>(
-        ne, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
+    k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s>>>(
+        nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
     ++launches;
   }
-  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(ne) * 32, 256), 256, 0, s>>>(
-      ne, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
+  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s>>>(
+      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
   ++launches;
   mark(7);
-  k_scatter<S><<<grid_for(d.dof_count(), 256), 256, 0, s>>>(d.dof_count(), d_dof_start_, d_dof_inc_, d_lsign_, loc, y);
+  k_scatter<S><<<grid_for(d.dof_count(), 256), 256, 0, s>>>(d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
   ++launches;
   mark(8);
   IGB_CUDA(cudaGetLastError());
+}
+
+template <class KT>
+void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cudaEvent_t* pev) {
+  int launches = 0;
+  enqueue_phase1<KT>(xin, nullptr, s, pev, launches);
+  enqueue_phase2<KT>(nullptr, yout, s, pev, launches);
   apply_launches_ = launches;
+}
+
+template <class F>
+void H2Device::dispatch_kind(F&& f) {
+  const int kind = disc_->kind();
+  const int q = kind == kMaxwell ? disc_->degree() : disc_->scalar_degree();
+  if (kind == kLaplace) {
+    switch (q) {
+      case 0: f(LapT<0>{}); break;
+      case 1: f(LapT<1>{}); break;
+      case 2: f(LapT<2>{}); break;
+      case 3: f(LapT<3>{}); break;
+      default: f(LapT<4>{}); break;
+    }
+  } else if (kind == kHelmholtz) {
+    switch (q) {
+      case 0: f(HelmT<0>{}); break;
+      case 1: f(HelmT<1>{}); break;
+      case 2: f(HelmT<2>{}); break;
+      case 3: f(HelmT<3>{}); break;
+      default: f(HelmT<4>{}); break;
+    }
+  } else {
+    switch (q) {
+      case 1: f(MaxT<1>{}); break;
+      case 2: f(MaxT<2>{}); break;
+      default: f(MaxT<3>{}); break;
+    }
+  }
+}
+
+void H2Device::dist_phase1(const double* x, double* send, cudaStream_t s) {
+  IGB_CUDA(cudaSetDevice(device_));
+  int n = 0;
+  dispatch_kind([&](auto kt) { enqueue_phase1<decltype(kt)>(x, send, s, nullptr, n); });
+  phase1_launches_ = n;
+}
+void H2Device::dist_phase2(const double* recv, double* y, cudaStream_t s) {
+  IGB_CUDA(cudaSetDevice(device_));
+  int n = 0;
+  dispatch_kind([&](auto kt) { enqueue_phase2<decltype(kt)>(recv, y, s, nullptr, n); });
+  apply_launches_ = phase1_launches_ + n;
 }
 
 void H2Device::enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev) {

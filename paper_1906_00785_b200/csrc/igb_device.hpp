@@ -23,8 +23,11 @@ class H2Device {
  public:
   // flags bit1 (IGB_H2_STORED_COUPLINGS): store the far couplings (reference
   // format) instead of evaluating them inside the matvec
+  // world > 1: this rank assembles and applies the block rows of its level-1
+  // clusters (build_local_plan); apply via dist_phase1 / all-gather /
+  // dist_phase2 / all-reduce
   H2Device(std::shared_ptr<const Discretization> d, int m, double eta, int far_order,
-           int sing_order, int device, int flags = 0);
+           int sing_order, int device, int flags = 0, int world = 1, int rank = 0);
   ~H2Device();
   H2Device(const H2Device&) = delete;
   H2Device& operator=(const H2Device&) = delete;
@@ -32,6 +35,13 @@ class H2Device {
   const Discretization& disc() const { return *disc_; }
   bool stored_couplings() const { return (flags_ & 2) != 0; }
   const H2Plan& plan() const { return plan_; }
+  const LocalPlan& local_plan() const { return lp_; }
+  // multi-GPU matvec: phase 1 (x -> packed owned up moments, `send` holds
+  // send_count() scalars), caller all-gathers into `recv` (world * send_count),
+  // phase 2 (recv -> partial y over all DOFs), caller all-reduces y
+  size_t send_count() const { return static_cast<size_t>(lp_.pack_max) * nch_ * plan_.m * plan_.m; }
+  void dist_phase1(const double* x, double* send, cudaStream_t s);
+  void dist_phase2(const double* recv, double* y, cudaStream_t s);
   bool is_complex() const { return disc_->is_complex(); }
   int dim() const { return disc_->dof_count(); }
   int nch() const { return nch_; }
@@ -70,10 +80,14 @@ class H2Device {
   template <class KT> void assemble_impl();
   template <class KT> void run_assembly();
   template <class KT> void enqueue_apply(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev);
+  template <class KT> void enqueue_phase1(const double* x, double* send, cudaStream_t s, cudaEvent_t* pev, int& n);
+  template <class KT> void enqueue_phase2(const double* recv, double* y, cudaStream_t s, cudaEvent_t* pev, int& n);
+  template <class F> void dispatch_kind(F&& f);
   void enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev);
 
   std::shared_ptr<const Discretization> disc_;
   H2Plan plan_;
+  LocalPlan lp_;
   int device_ = 0, nch_ = 1, flags_ = 0;
   cudaStream_t stream_ = nullptr;
   AssemblyTimes times_;
@@ -103,6 +117,9 @@ class H2Device {
   double* d_slot_ = nullptr;
   int *d_far_a_ = nullptr;
   int *d_dof_start_ = nullptr, *d_dof_inc_ = nullptr;
+  int *d_near_ea_ = nullptr, *d_el_ = nullptr, *d_pack_nodes_ = nullptr, *d_unpack_nodes_ = nullptr;
+  unsigned char* d_owned_ = nullptr;
+  double *d_loc_sign_ = nullptr, *d_send_ = nullptr, *d_recv_ = nullptr;
   double *d_tl_ = nullptr, *d_tr_ = nullptr;
   // operator data
   double* d_near_ = nullptr;   // row layout [e][la][k][lb], Scalar
@@ -119,7 +136,7 @@ class H2Device {
   cudaStream_t side_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
-  int apply_launches_ = 0;
+  int apply_launches_ = 0, phase1_launches_ = 0;
   int assembly_kernels_ = 0, assembly_launches_count_ = 0;
   size_t upload_bytes_ = 0;
   struct AsmState {

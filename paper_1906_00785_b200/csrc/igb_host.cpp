@@ -1187,4 +1187,82 @@ RowPartition partition_rows(const Discretization& d, const H2Plan& P, int world,
   return r;
 }
 
+LocalPlan build_local_plan(const Discretization& d, const H2Plan& P, int world, int rank) {
+  LocalPlan Lp;
+  Lp.world = world;
+  Lp.rank = rank;
+  const int ne = d.element_count(), nl = d.local_count(), nn = P.n_nodes;
+  std::vector<RowPartition> parts;
+  for (int r = 0; r < world; ++r) parts.push_back(partition_rows(d, P, world, r));
+  const RowPartition& me = parts[rank];
+  Lp.c0 = me.c0;
+  Lp.c1 = me.c1;
+  Lp.el = me.elements;
+  Lp.el_local.assign(ne, -1);
+  for (size_t i = 0; i < Lp.el.size(); ++i) Lp.el_local[Lp.el[i]] = static_cast<int>(i);
+  // near rows
+  const long long nnear = static_cast<long long>(P.near_a.size());
+  Lp.slot_local.assign(nnear, -1);
+  Lp.near_rs.assign(Lp.el.size() + 1, 0);
+  for (size_t i = 0; i < Lp.el.size(); ++i) {
+    const int e = Lp.el[i];
+    Lp.near_rs[i + 1] = Lp.near_rs[i] + (P.near_row_start[e + 1] - P.near_row_start[e]);
+    for (int q = P.near_row_start[e]; q < P.near_row_start[e + 1]; ++q) {
+      Lp.slot_local[q] = static_cast<int>(Lp.near_row.size());
+      Lp.near_row.push_back(static_cast<int>(i));
+      Lp.near_ea.push_back(e);
+      Lp.near_eb.push_back(P.near_b[q]);
+    }
+  }
+  for (int c = 1; c <= 3; ++c) {
+    const auto& G = P.sing[c];
+    auto& L = Lp.sing[c];
+    for (size_t k = 0; k < G.ea.size(); ++k) {
+      const int sab = Lp.slot_local[G.slot_ab[k]], sba = Lp.slot_local[G.slot_ba[k]];
+      if (sab < 0 && sba < 0) continue;
+      L.ea.push_back(G.ea[k]);
+      L.eb.push_back(G.eb[k]);
+      L.map_a.push_back(G.map_a[k]);
+      L.map_b.push_back(G.map_b[k]);
+      L.slot_ab.push_back(sab);
+      L.slot_ba.push_back(G.slot_ba[k] == G.slot_ab[k] ? sab : sba);
+    }
+  }
+  for (int q : P.reg_slot)
+    if (Lp.slot_local[q] >= 0) Lp.reg_slot.push_back(Lp.slot_local[q]);
+  // tree nodes
+  Lp.node_owned.assign(nn, 0);
+  Lp.rank_pack_nodes.assign(world, {});
+  for (int t = 0; t < nn; ++t) {
+    const int cl = node_cluster(P, t);
+    if (cl < 0) {
+      Lp.node_owned[t] = 1;  // roots: replicated on every rank
+      continue;
+    }
+    for (int r = 0; r < world; ++r)
+      if (cl >= parts[r].c0 && cl < parts[r].c1) {
+        Lp.rank_pack_nodes[r].push_back(t);
+        if (r == rank) Lp.node_owned[t] = 1;
+      }
+  }
+  Lp.pack_nodes = Lp.rank_pack_nodes[rank];
+  for (const auto& v : Lp.rank_pack_nodes) Lp.pack_max = std::max<int>(Lp.pack_max, static_cast<int>(v.size()));
+  for (int t = 0; t < nn; ++t)
+    if (Lp.node_owned[t] && P.far_row_start[t + 1] > P.far_row_start[t]) Lp.far_targets.push_back(t);
+  // DOF gather over owned elements, ascending (e, l)
+  const int nd = d.dof_count();
+  Lp.dof_start.assign(nd + 1, 0);
+  for (int e : Lp.el)
+    for (int l = 0; l < nl; ++l) ++Lp.dof_start[d.l2g()[static_cast<size_t>(e) * nl + l] + 1];
+  for (int i = 0; i < nd; ++i) Lp.dof_start[i + 1] += Lp.dof_start[i];
+  Lp.dof_inc.resize(Lp.dof_start[nd]);
+  std::vector<int> fillp(Lp.dof_start.begin(), Lp.dof_start.end() - 1);
+  for (size_t i = 0; i < Lp.el.size(); ++i)
+    for (int l = 0; l < nl; ++l) {
+      const int e = Lp.el[i];
+      Lp.dof_inc[fillp[d.l2g()[static_cast<size_t>(e) * nl + l]]++] = static_cast<int>(i) * nl + l;
+    }
+  return Lp;
+}
+
 }  // namespace igb

@@ -248,4 +248,26 @@ struct RowPartition {
 int node_cluster(const H2Plan& P, int node);  // level-1 cluster of a node, -1 for roots
 RowPartition partition_rows(const Discretization& d, const H2Plan& P, int world, int rank);
 
+// Rank-local view of the plan (identity for world == 1): owned block rows,
+// their near slots, singular / regular work items touching them, owned tree
+// nodes and far targets, and the pack lists of the up-moment all-gather.
+struct LocalPlan {
+  int world = 1, rank = 0, c0 = 0, c1 = 0;
+  std::vector<int> el;                 // owned elements (global ids, ascending)
+  std::vector<int> el_local;           // global -> local element index, -1 if not owned
+  std::vector<int> near_rs;            // local rows: slot starts (n_owned + 1)
+  std::vector<int> near_row;           // per local slot: local row
+  std::vector<int> near_ea, near_eb;   // per local slot: global elements
+  std::vector<int> slot_local;         // global slot -> local slot or -1
+  H2Plan::SingList sing[4];            // items touching owned rows; slots local or -1
+  std::vector<int> reg_slot;           // local slots of owned regular pairs
+  std::vector<unsigned char> node_owned;  // per node (roots owned by every rank)
+  std::vector<int> far_targets;        // owned nodes with far pairs (ascending)
+  std::vector<int> pack_nodes;         // owned nodes at levels >= 1 (ascending): all-gather payload
+  std::vector<std::vector<int>> rank_pack_nodes;  // per rank (for unpacking)
+  int pack_max = 0;                    // max payload nodes over ranks
+  std::vector<int> dof_start, dof_inc; // gather of owned (local e * nl + l) per DOF
+};
+LocalPlan build_local_plan(const Discretization& d, const H2Plan& P, int world, int rank);
+
 }  // namespace igb

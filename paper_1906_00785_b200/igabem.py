@@ -72,13 +72,14 @@ class _PatchDesc(ctypes.Structure):
 SYMBOLS = (
     "igb_geometry_create", "igb_geometry_sphere", "igb_geometry_square", "igb_geometry_info",
     "igb_geometry_destroy", "igb_discretization_create", "igb_discretization_info", "igb_discretization_l2g",
-    "igb_discretization_elements", "igb_classify_pair", "igb_discretization_destroy", "igb_h2_create", "igb_h2_create_ex",
+    "igb_discretization_elements", "igb_classify_pair", "igb_discretization_destroy", "igb_h2_create", "igb_h2_create_ex", "igb_h2_create_dist", "igb_h2_dist_send_count",
+    "igb_h2_dist_phase1", "igb_h2_dist_phase2",
     "igb_h2_dim", "igb_h2_apply", "igb_h2_apply_device", "igb_h2_storage_report", "igb_h2_counts",
     "igb_h2_near_pairs", "igb_h2_far_pairs", "igb_h2_tree", "igb_h2_near_blocks", "igb_h2_couplings",
     "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
     "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_counts", "igb_plan_near_pairs",
-    "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
+    "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
 )
 
 
@@ -111,6 +112,10 @@ def lib():
     L.igb_discretization_destroy.restype = None
     L.igb_h2_create.argtypes = [vp, P(_Opts), i32, P(vp)]
     L.igb_h2_create_ex.argtypes = [vp, P(_Opts), i32, i32, P(vp)]
+    L.igb_h2_create_dist.argtypes = [vp, P(_Opts), i32, i32, i32, i32, P(vp)]
+    L.igb_h2_dist_send_count.argtypes = [vp, P(sz)]
+    L.igb_h2_dist_phase1.argtypes = [vp, vp, vp, vp]
+    L.igb_h2_dist_phase2.argtypes = [vp, vp, vp, vp]
     L.igb_h2_dim.argtypes = [vp, P(i32)]
     L.igb_h2_apply.argtypes = [vp, P(f64), P(f64)]
     L.igb_h2_apply_device.argtypes = [vp, vp, vp, vp]
@@ -140,6 +145,7 @@ def lib():
     L.igb_plan_far_pairs.argtypes = [vp, P(i32)]
     L.igb_plan_class_counts.argtypes = [vp, P(i64)]
     L.igb_plan_partition.argtypes = [vp, i32, i32, P(i32), P(i32), P(i32), P(i64), P(i64)]
+    L.igb_plan_owned.argtypes = [vp, i32, i32, P(ctypes.c_ubyte), P(ctypes.c_ubyte)]
     L.igb_plan_destroy.argtypes = [vp]
     L.igb_plan_destroy.restype = None
     L.igb_admissible.argtypes = [P(f64), P(f64), f64]
@@ -381,6 +387,13 @@ class H2Plan:
                                         ctypes.byref(ne), ctypes.byref(nn), ctypes.byref(nf)))
         return dict(clusters=(c0.value, c1.value), elements=ne.value, near=nn.value, far=nf.value)
 
+    def owned(self, world, rank, n_elements):
+        """(element mask, node mask) of one rank of the row-cluster partition"""
+        em = np.zeros(n_elements, dtype=np.uint8)
+        nm = np.zeros(self.node_count, dtype=np.uint8)
+        _check(lib().igb_plan_owned(self._h, int(world), int(rank), _p(em, ctypes.c_ubyte), _p(nm, ctypes.c_ubyte)))
+        return em.astype(bool), nm.astype(bool)
+
 
 class H2Matrix:
     """H2Matrix<Scalar>(disc, opts) (h2.hpp:57-106), assembled and applied on a B200.
@@ -389,12 +402,17 @@ class H2Matrix:
     complex128 for Helmholtz / Maxwell), like the reference's Eigen vectors."""
 
     def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int = 0,
-                 stored_couplings: bool = False):
+                 stored_couplings: bool = False, world: int = 1, rank: int = 0):
         opts = opts or H2Options()
         o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
         h = ctypes.c_void_p()
         flags = 2 if stored_couplings else 0
-        _check(lib().igb_h2_create_ex(disc._h, ctypes.byref(o), int(device), flags, ctypes.byref(h)))
+        if world == 1:
+            _check(lib().igb_h2_create_ex(disc._h, ctypes.byref(o), int(device), flags, ctypes.byref(h)))
+        else:
+            _check(lib().igb_h2_create_dist(disc._h, ctypes.byref(o), int(device), flags, int(world), int(rank),
+                                            ctypes.byref(h)))
+        self.world, self.rank, self.device = world, rank, device
         self.stored_couplings = stored_couplings
         self._h = h
         self._disc = disc
@@ -430,6 +448,20 @@ class H2Matrix:
         """Device-pointer matvec (x, y: CUDA device addresses of rows() scalars)."""
         _check(lib().igb_h2_apply_device(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr),
                                          ctypes.c_void_p(stream or None)))
+
+    # multi-GPU phases (device pointers, cudaStream_t as int) -------------------
+    def dist_send_count(self):
+        n = ctypes.c_size_t()
+        _check(lib().igb_h2_dist_send_count(self._h, ctypes.byref(n)))
+        return n.value
+
+    def dist_phase1(self, x_ptr, send_ptr, stream=0):
+        _check(lib().igb_h2_dist_phase1(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(send_ptr),
+                                        ctypes.c_void_p(stream or None)))
+
+    def dist_phase2(self, recv_ptr, y_ptr, stream=0):
+        _check(lib().igb_h2_dist_phase2(self._h, ctypes.c_void_p(recv_ptr), ctypes.c_void_p(y_ptr),
+                                        ctypes.c_void_p(stream or None)))
 
     def storage_report(self) -> H2Storage:
         s = _Storage()
@@ -531,3 +563,37 @@ class H2Matrix:
         launches = ctypes.c_int()
         _check(lib().igb_h2_bench_apply(self._h, int(iters), ctypes.byref(ms), ctypes.byref(launches)))
         return ms.value, launches.value
+
+
+class DistH2Matrix:
+    """Row-cluster-partitioned H2Matrix on one rank of a torch.distributed
+    (NCCL) job: each rank assembles the block rows of its
+    level-1 clusters; a matvec all-gathers the level>=1 up moments and
+    all-reduces the partial result.  x and y are device tensors (replicated)."""
+
+    def __init__(self, disc, opts=None, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        dev = torch.cuda.current_device() if device is None else device
+        self.h = H2Matrix(disc, opts, device=dev, world=self.world, rank=self.rank)
+        self.dtype = torch.complex128 if self.h.dtype == np.complex128 else torch.float64
+        n = self.h.dist_send_count()
+        self.send = torch.zeros(max(n, 1), dtype=self.dtype, device=f"cuda:{dev}")
+        self.recv = torch.zeros(max(n, 1) * self.world, dtype=self.dtype, device=f"cuda:{dev}")
+        self.n = n
+
+    def rows(self):
+        return self.h.rows()
+
+    def apply(self, x, y=None):
+        torch = self.torch
+        y = torch.empty_like(x) if y is None else y
+        stream = torch.cuda.current_stream().cuda_stream
+        self.h.dist_phase1(x.data_ptr(), self.send.data_ptr(), stream)
+        self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        self.h.dist_phase2(self.recv.data_ptr(), y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        self.dist.all_reduce(y, group=self.group)
+        return y
