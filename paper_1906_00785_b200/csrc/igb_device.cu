@@ -1002,8 +1002,10 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 template <int M>
 struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static constexpr int MM = M * M;
-  static constexpr int BR = (M == 3) ? 3 : (M == 5 ? 5 : 4);
-  static constexpr int BC = (M == 2) ? 4 : (M == 3 ? 9 : (M == 5 ? 6 : 8));
+  // m = 4: 4 x 8 lanes (A/B on B200: 0.37 ms vs 0.41 ms for 2 x 16 at c2);
+  // m = 5: 2 x 16 (no spills at 1 block/SM)
+  static constexpr int BR = (M == 5) ? 2 : (M == 3 ? 3 : 4);
+  static constexpr int BC = (M == 5) ? 16 : (M == 2 ? 4 : (M == 3 ? 9 : 8));
   static constexpr int RN = (MM + BR - 1) / BR, CN = (MM + BC - 1) / BC;
   static_assert(BR * BC <= 32, "lane grid");
 };
@@ -1013,7 +1015,7 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
 // gives down[t] += K up[s] (accumulated in registers) and K^T up[t], written to
 // the slot of the transposed pair (s, t) and summed by k_far_lower in fixed
 // order.  Lane (bi, bj) owns RN target rows x CN source columns.
-template <int M, bool PF, int MINB>
+template <int M, bool DIST, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int* __restrict__ targets,
                                                  const int* __restrict__ upper_start, const int* __restrict__ far_rs,
                                                  const int* __restrict__ far_b, const int* __restrict__ trans,
@@ -1043,9 +1045,7 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
   // pairs (t, s): s > t and s owned -> symmetric (t's row + slot of (s, t));
   // s not owned (other rank's block rows) -> one-sided; s < t owned -> skip
   // (evaluated by s's warp).  Single GPU: every s owned, only s > t visited.
-  const int q0 = full_row ? far_rs[t] : upper_start[t], q1 = far_rs[t + 1];
-  // software pipeline: the next source cluster's images/moments are loaded
-  // while the current one is evaluated
+  const int q0 = (DIST && full_row) ? far_rs[t] : upper_start[t], q1 = far_rs[t + 1];
   double nsx[CN][3], nxs[CN];
   auto load = [&](int q) {
     const int s = far_b[q];
@@ -1060,13 +1060,15 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
       nxs[j] = ok ? __ldg(up + static_cast<size_t>(s) * MM + mu) : 0.0;
     }
   };
-  if (PF && q0 < q1) load(q0);
   for (int q = q0; q < q1; ++q) {
-    const int sq = far_b[q];
-    const bool own_s = owned[sq] != 0;
-    if (own_s && sq < t) continue;  // warp-uniform
+    bool own_s = true;
+    if constexpr (DIST) {
+      const int sq = far_b[q];
+      own_s = owned[sq] != 0;
+      if (own_s && sq < t) continue;  // warp-uniform
+    }
     double sx[CN][3], xs[CN], ps[CN];
-    if (!PF) load(q);
+    load(q);
 #pragma unroll
     for (int j = 0; j < CN; ++j) {
       sx[j][0] = nsx[j][0];
@@ -1075,7 +1077,6 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
       xs[j] = nxs[j];
       ps[j] = 0.0;
     }
-    if (PF && q + 1 < q1) load(q + 1);
 #pragma unroll
     for (int i = 0; i < RN; ++i)
 #pragma unroll
@@ -1085,7 +1086,7 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
         acc[i] = fma(gk, xs[j], acc[i]);
         ps[j] = fma(gk, xt[i], ps[j]);
       }
-    if (!own_s) continue;  // one-sided pair: no transposed product
+    if (DIST && !own_s) continue;  // one-sided pair: no transposed product
     // K^T up[t] for the CN columns: reduce over the BR lanes of the column
 #pragma unroll
     for (int j = 0; j < CN; ++j) {
@@ -1828,14 +1829,18 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
       double* dn = reinterpret_cast<double*>(down);
       const double* upd = reinterpret_cast<const double*>(up);
 #define IGB_FS(MM_, MB_)                                                                                        \
-  k_far_sym<MM_, false, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,        \
+  if (lp_.world > 1)                                                                                           \
+    k_far_sym<MM_, true, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,       \
+                                                d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 1);     \
+  else                                                                                                         \
+    k_far_sym<MM_, false, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,        \
                                                  d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, \
                                                  d_owned_, lp_.world > 1 ? 1 : 0)
       switch (m) {  // occupancy chosen so no variant spills (ptxas -warn-spills)
         case 2: IGB_FS(2, 3); break;
         case 3: IGB_FS(3, 3); break;
         case 4: IGB_FS(4, 3); break;
-        case 5: IGB_FS(5, 2); break;
+        case 5: IGB_FS(5, 1); break;
         default: IGB_FS(6, 1); break;
       }
 #undef IGB_FS
