@@ -197,6 +197,33 @@ int igb_plan_partition(const igb_plan* p, int world, int rank, int* c0, int* c1,
 int igb_plan_owned(const igb_plan* p, int world, int rank, unsigned char* element_owned, unsigned char* node_owned);
 void igb_plan_destroy(igb_plan* p);
 
+/* ---- around the operator ---- */
+/* SolverOptions / SolveStats (solver.hpp:37-48) */
+typedef struct {
+  double tol;
+  int max_iter;
+  int restart;
+} igb_solver_opts;
+typedef struct {
+  int iterations;
+  double residual;
+  int converged;
+  double seconds;
+} igb_solve_stats;
+/* gmres(LinearOperator{h.apply}, b) (solver.hpp:54-155) and cg (159-200),
+ * device-resident vectors; b, x host buffers of rows() scalars */
+int igb_h2_gmres(igb_h2* h, const double* b, double* x, const igb_solver_opts* opts, igb_solve_stats* stats);
+int igb_h2_cg(igb_h2* h, const double* b, double* x, const igb_solver_opts* opts, igb_solve_stats* stats);
+/* load vectors (assembly.cpp:55-133): the quadrature points of every element
+ * (element-major, *n_per_element points each, xyz), then b from the data
+ * values at those points (one Scalar per point; Maxwell: 3 complex) */
+int igb_rhs_points(const igb_discretization* d, int quad_order, int device, double* pts, int* n_per_element);
+int igb_rhs_assemble(const igb_discretization* d, int quad_order, int device, const double* values, double* b);
+/* eval_potential / eval_maxwell_potential (operators.cpp:112-208); out: one
+ * Scalar per point, Maxwell 3 complex per point */
+int igb_potential(const igb_discretization* d, const double* density, int n_points, const double* points,
+                  int quad_order, int device, double* out);
+
 /* eta-admissibility of two boxes (min xyz, max xyz), h2.cpp:92-97 */
 int igb_admissible(const double box_a[6], const double box_b[6], double eta);
 int igb_last_error(char* buf, size_t n);

@@ -28,12 +28,12 @@ class _Prefixed:
         return f
 
 
-def _sig(L, name, argtypes):
+def _sig(L, name, argtypes, optional=False):
     try:
         getattr(L, name).argtypes = argtypes
     except AttributeError:
-        if PREFIX == "orc_":
-            raise  # the restatement must export everything; the reference harness a subset
+        if PREFIX == "orc_" and not optional:
+            raise  # the restatement must export the path; the reference harness a subset
 
 
 LIB_PATH = os.path.join(_HERE, "liborc.so")
@@ -78,6 +78,10 @@ def lib():
         _sig(L, "orc_gauss", [i32, P(f64), P(f64)])
         _sig(L, "orc_pair_rule", [i32, i32, P(f64), P(i64)])
         _sig(L, "orc_admissible", [P(f64), P(f64), f64])
+        # 8(f) pipeline: exported by the reference harness (oracle/_ref) only
+        _sig(L, "orc_rhs", [vp, i32, P(f64), i32, P(f64)], optional=True)
+        _sig(L, "orc_solve", [vp, i32, P(f64), f64, i32, i32, P(f64), P(f64)], optional=True)
+        _sig(L, "orc_potential", [vp, P(f64), i32, P(f64), i32, P(f64)], optional=True)
         _sig(L, "orc_last_error", [ctypes.c_char_p, i32])
         _LIB = L
     return _LIB
@@ -200,6 +204,22 @@ class Discretization:
         # stored column-major per block: transpose to [la, lb]
         return np.ascontiguousarray(out.transpose(0, 2, 1))
 
+    def rhs(self, data, params, order=0):
+        """reference compute_rhs* for built-in data (see oracle/ref_harness.cpp ref_rhs)"""
+        q = np.zeros(6)
+        q[:len(params)] = params
+        b = np.zeros(self.dof_count, dtype=self.dtype)
+        _check(lib().orc_rhs(self._h, int(data), _p(q), int(order), _p(b.view(np.float64))))
+        return b
+
+    def potential(self, density, pts, order=10):
+        dens = np.ascontiguousarray(density, dtype=self.dtype)
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        out = np.zeros((len(pts), 3) if self.kind == "maxwell" else len(pts), dtype=self.dtype)
+        _check(lib().orc_potential(self._h, _p(dens.view(np.float64)), len(pts), _p(pts), int(order),
+                                   _p(out.view(np.float64))))
+        return out
+
     def assemble_dense(self, far_order=0, sing_order=0):
         nd = self.dof_count
         a = np.zeros((nd, nd), dtype=self.dtype)
@@ -238,6 +258,15 @@ class H2Matrix:
         return y
 
     __matmul__ = apply
+
+    def solve(self, b, method="gmres", tol=1e-8, max_iter=1000, restart=30):
+        """reference gmres / cg (solver.hpp) on this H2Matrix"""
+        b = np.ascontiguousarray(b, dtype=self.dtype)
+        x = np.zeros_like(b)
+        st = np.zeros(4)
+        _check(lib().orc_solve(self._h, 0 if method == "gmres" else 1, _p(b.view(np.float64)), float(tol),
+                               int(max_iter), int(restart), _p(x.view(np.float64)), _p(st)))
+        return x, dict(iterations=int(st[0]), residual=float(st[1]), converged=bool(st[2]), seconds=float(st[3]))
 
     def nearfield_pairs(self):
         out = np.zeros((self.near_count, 2), dtype=np.int32)

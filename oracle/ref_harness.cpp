@@ -306,6 +306,91 @@ int ref_h2_apply(void* hp, const double* x, double* y) {
     }
   });
 }
+// load vectors with the reference's compute_rhs* (assembly.cpp:108-133) for
+// built-in data: 0 Laplace point source at q[0..2]; 1 Helmholtz point source
+// (reference kernel e^{-i k r}/(4 pi r)); 2 Maxwell dipole at q[0..2] with
+// moment q[3..5]; 3 Maxwell plane wave E = -pol e^{-i k d.x}, d = q[0..2],
+// pol = q[3..5]; 4 outgoing e^{+i k r}/(4 pi r) point source
+int ref_rhs(void* dp, int data, const double* q, int order, double* out) {
+  return guard([&] {
+    const Discretization& d = *static_cast<RDisc*>(dp)->disc;
+    const Eigen::Vector3d a(q[0], q[1], q[2]), bq(q[3], q[4], q[5]);
+    const cplx kap = d.pde().kappa;
+    if (data == 0) {
+      const auto b = compute_rhs(d, [&](const Eigen::Vector3d& x) { return laplace_point_source(x, a); }, order);
+      std::memcpy(out, b.data(), sizeof(double) * b.size());
+    } else if (data == 1 || data == 4) {
+      const auto b = compute_rhs_complex(
+          d,
+          [&](const Eigen::Vector3d& x) {
+            const cplx v = helmholtz_point_source(x, a, kap);
+            return data == 1 ? v : std::conj(v);
+          },
+          order);
+      std::memcpy(out, b.data(), sizeof(cplx) * b.size());
+    } else {
+      const auto b = compute_rhs_maxwell(
+          d,
+          [&](const Eigen::Vector3d& x) -> Eigen::Vector3cd {
+            if (data == 2) return maxwell_dipole(x, a, bq, kap);
+            const cplx ph = std::exp(cplx(0, -1) * kap * a.dot(x));
+            return -(ph * bq.cast<cplx>());
+          },
+          order);
+      std::memcpy(out, b.data(), sizeof(cplx) * b.size());
+    }
+  });
+}
+// gmres (method 0) or cg (1) of solver.hpp on the reference H2Matrix
+int ref_solve(void* hp, int method, const double* b, double tol, int max_iter, int restart, double* x,
+              double* stats) {
+  return guard([&] {
+    RH2* h = static_cast<RH2*>(hp);
+    const int n = h->d->disc->dof_count();
+    SolverOptions o{tol, max_iter, restart};
+    auto run = [&](auto& H, auto tag) {
+      using S = decltype(tag);
+      using Vec = Eigen::Matrix<S, Eigen::Dynamic, 1>;
+      Vec bv(n);
+      std::memcpy(bv.data(), b, sizeof(S) * n);
+      LinearOperator<S> op{n, [&H](const Vec& v) { return H.apply(v); }};
+      auto [xv, st] = method == 0 ? gmres(op, bv, o) : cg(op, bv, o);
+      std::memcpy(x, xv.data(), sizeof(S) * n);
+      stats[0] = st.iterations;
+      stats[1] = st.residual;
+      stats[2] = st.converged ? 1 : 0;
+      stats[3] = st.seconds;
+    };
+    if (h->real) run(*h->real, double{}); else run(*h->cx, cplx{});
+  });
+}
+// eval_potential / eval_maxwell_potential (operators.cpp:112-208)
+int ref_potential(void* dp, const double* dens, int npts, const double* pts, int order, double* out) {
+  return guard([&] {
+    const Discretization& d = *static_cast<RDisc*>(dp)->disc;
+    std::vector<Eigen::Vector3d> p(npts);
+    for (int i = 0; i < npts; ++i) p[i] = Eigen::Vector3d(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    const int n = d.dof_count();
+    if (!d.pde().is_complex()) {
+      Eigen::VectorXd rho(n);
+      std::memcpy(rho.data(), dens, sizeof(double) * n);
+      const auto u = eval_potential(d, rho, p, order);
+      std::memcpy(out, u.data(), sizeof(double) * npts);
+    } else {
+      Eigen::VectorXcd rho(n);
+      std::memcpy(rho.data(), dens, sizeof(cplx) * n);
+      if (d.pde().is_vector()) {
+        const auto e = eval_maxwell_potential(d, rho, p, order);
+        for (int i = 0; i < npts; ++i)
+          for (int k = 0; k < 3; ++k) reinterpret_cast<cplx*>(out)[3 * i + k] = e(k, i);
+      } else {
+        const auto u = eval_potential(d, rho, p, order);
+        std::memcpy(out, u.data(), sizeof(cplx) * npts);
+      }
+    }
+  });
+}
+
 int ref_admissible(const double* boxa, const double* boxb, double eta) {
   ClusterNode a{0, 0, 0, 0, {}}, b{0, 0, 0, 0, {}};
   a.box = Eigen::AlignedBox3d(Eigen::Vector3d(boxa[0], boxa[1], boxa[2]), Eigen::Vector3d(boxa[3], boxa[4], boxa[5]));

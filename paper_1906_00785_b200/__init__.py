@@ -6,8 +6,10 @@ reference API.  See DESIGN.md.
 """
 from .igabem import (AssemblyOptions, COINCIDENT, DomainError, EDGE, FAR, Geometry, H2Matrix, H2Options,
                      H2Storage, HELMHOLTZ, LAPLACE, LogicError, MAXWELL, Pde, VERTEX, CudaError,
-                     Discretization, DistH2Matrix, H2Plan, admissible, lib, library_path, make_sphere, make_square, SYMBOLS)
+                     Discretization, DistH2Matrix, H2Plan, admissible, SolverOptions, SolveStats, gmres, cg,
+                     quadrature_points, compute_rhs, eval_potential, eval_maxwell_potential, make_sphere_grid, lib, library_path, make_sphere, make_square, SYMBOLS)
 
 __all__ = ["AssemblyOptions", "Geometry", "H2Matrix", "H2Options", "H2Storage", "Pde", "Discretization", "DistH2Matrix", "H2Plan",
-           "admissible", "make_sphere", "make_square", "lib", "library_path", "LogicError", "DomainError",
+           "admissible", "SolverOptions", "SolveStats", "gmres", "cg", "quadrature_points",
+           "compute_rhs", "eval_potential", "eval_maxwell_potential", "make_sphere_grid", "make_sphere", "make_square", "lib", "library_path", "LogicError", "DomainError",
            "CudaError", "LAPLACE", "HELMHOLTZ", "MAXWELL", "FAR", "VERTEX", "EDGE", "COINCIDENT", "SYMBOLS"]

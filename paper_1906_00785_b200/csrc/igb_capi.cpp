@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/igabem_b200.h"
+#include "igb_apps.hpp"
 #include "igb_device.hpp"
 #include "igb_host.hpp"
 
@@ -513,6 +514,58 @@ int igb_plan_owned(const igb_plan* p, int world, int rank, unsigned char* elemen
   });
 }
 void igb_plan_destroy(igb_plan* p) { delete p; }
+
+int igb_h2_gmres(igb_h2* h, const double* b, double* x, const igb_solver_opts* opts, igb_solve_stats* stats) {
+  return guard([&] {
+    need(h, "h2");
+    need(b, "b");
+    need(x, "x");
+    igb::SolverOpts o;
+    if (opts) o = igb::SolverOpts{opts->tol, opts->max_iter, opts->restart};
+    const auto r = igb::gmres(*h->dev, b, x, o);
+    if (stats) *stats = igb_solve_stats{r.iterations, r.residual, r.converged ? 1 : 0, r.seconds};
+  });
+}
+int igb_h2_cg(igb_h2* h, const double* b, double* x, const igb_solver_opts* opts, igb_solve_stats* stats) {
+  return guard([&] {
+    need(h, "h2");
+    need(b, "b");
+    need(x, "x");
+    igb::SolverOpts o;
+    if (opts) o = igb::SolverOpts{opts->tol, opts->max_iter, opts->restart};
+    const auto r = igb::cg(*h->dev, b, x, o);
+    if (stats) *stats = igb_solve_stats{r.iterations, r.residual, r.converged ? 1 : 0, r.seconds};
+  });
+}
+int igb_rhs_points(const igb_discretization* d, int quad_order, int device, double* pts, int* n_per_element) {
+  return guard([&] {
+    need(d, "discretization");
+    const int n = quad_order > 0 ? quad_order : d->d->degree() + 2;
+    if (n_per_element) *n_per_element = n * n;
+    if (pts) {
+      std::vector<double> v;
+      igb::quad_points(*d->d, quad_order, device, v);
+      std::memcpy(pts, v.data(), v.size() * sizeof(double));
+    }
+  });
+}
+int igb_rhs_assemble(const igb_discretization* d, int quad_order, int device, const double* values, double* b) {
+  return guard([&] {
+    need(d, "discretization");
+    need(values, "values");
+    need(b, "b");
+    igb::assemble_rhs(*d->d, quad_order, device, values, b);
+  });
+}
+int igb_potential(const igb_discretization* d, const double* density, int n_points, const double* points,
+                  int quad_order, int device, double* out) {
+  return guard([&] {
+    need(d, "discretization");
+    need(density, "density");
+    if (n_points < 0) throw std::invalid_argument("eval_potential: negative point count");
+    igb::eval_potential(*d->d, quad_order, device, density, n_points, points, out);
+  });
+}
 
 int igb_admissible(const double a[6], const double b[6], double eta) {
   igb::Box A, B;

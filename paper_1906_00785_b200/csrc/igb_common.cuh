@@ -1,0 +1,298 @@
+// Shared sm_100a device helpers: FP64 / complex scalars, Green's functions
+// (operators.hpp:16-20), rational geometry jets on the power-basis cells, and
+// the B-spline / Piola shape functions (spaces.cpp:257-307).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#define IGB_CUDA(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      throw std::runtime_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" + \
+                               #x + ")");                                                    \
+  } while (0)
+
+namespace igb {
+namespace dev {
+
+constexpr double kInv4Pi = 0.079577471545947667884;  // 1 / (4 pi)
+constexpr int kCellStride = 104;                       // 100 coefficients + u0, v0 (+pad)
+
+// ------------------------------------------------------------ scalars
+struct __align__(16) cd {
+  double x, y;
+};
+__host__ __device__ __forceinline__ cd mk(double a, double b) {
+  cd r;
+  r.x = a;
+  r.y = b;
+  return r;
+}
+template <class S>
+__device__ __forceinline__ S zero();
+template <>
+__device__ __forceinline__ double zero<double>() { return 0.0; }
+template <>
+__device__ __forceinline__ cd zero<cd>() { return mk(0.0, 0.0); }
+
+__device__ __forceinline__ double operator_add(double a, double b) { return a + b; }
+__device__ __forceinline__ cd operator+(cd a, cd b) { return mk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cd operator*(cd a, cd b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ cd operator*(cd a, double b) { return mk(a.x * b, a.y * b); }
+__device__ __forceinline__ cd operator*(double b, cd a) { return mk(a.x * b, a.y * b); }
+
+__device__ __forceinline__ void fmac(double& acc, double a, double b) { acc = fma(a, b, acc); }
+__device__ __forceinline__ void fmac(cd& acc, cd a, double b) {
+  acc.x = fma(a.x, b, acc.x);
+  acc.y = fma(a.y, b, acc.y);
+}
+__device__ __forceinline__ void fmac(cd& acc, double a, cd b) { fmac(acc, b, a); }
+__device__ __forceinline__ void fmac(cd& acc, cd a, cd b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ double shfl_down(double v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ cd shfl_down(cd v, int o) {
+  return mk(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
+}
+__device__ __forceinline__ double shfl_idx(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ cd shfl_idx(cd v, int src) {
+  return mk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ double ldg_s(const double* p) { return __ldg(p); }
+__device__ __forceinline__ cd ldg_s(const cd* p) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  return mk(v.x, v.y);
+}
+template <class S>
+__device__ __forceinline__ S warp_sum(S v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = v + shfl_down(v, o);
+  return v;  // valid in lane 0
+}
+
+// ------------------------------------------------------ kernel traits
+struct KParams {
+  double kr, ki;      // wavenumber
+  double dwx, dwy;    // -1/kappa^2 (Maxwell divergence weight)
+};
+template <int Q_>
+struct LapT {
+  using S = double;
+  static constexpr int KIND = 0, Q = Q_, NL = (Q_ + 1) * (Q_ + 1), NC = 1, CHUNK = 128;
+  static constexpr int TS = Q_ + 1;                  // accumulation tile side
+  static constexpr int TABN = 2 * (Q_ + 1) * (Q_ + 1);  // per element: u and v tables
+};
+template <int Q_>
+struct HelmT {
+  using S = cd;
+  static constexpr int KIND = 1, Q = Q_, NL = (Q_ + 1) * (Q_ + 1), NC = 1, CHUNK = 128;
+  static constexpr int TS = Q_ + 1;
+  static constexpr int TABN = 2 * (Q_ + 1) * (Q_ + 1);
+};
+template <int P_>
+struct MaxT {
+  using S = cd;
+  static constexpr int KIND = 2, Q = P_, NL = 2 * (P_ + 1) * P_, NC = 4, CHUNK = 64;
+  static constexpr int TS = (NL % 4 == 0) ? 4 : 2;
+  // per element: p-tables (u, v) of (P+1)^2 and q-tables (u, v) of P^2, padded even
+  static constexpr int TABN = ((2 * (P_ + 1) * (P_ + 1) + 2 * P_ * P_) + 1) / 2 * 2;
+};
+
+// Green's functions (operators.hpp:16-20), distance clamped as in
+// pair_integration.hpp:18,118
+__device__ __forceinline__ double green(double r2, const KParams&, double) {
+  double rinv = rsqrt(r2);
+  if (r2 < 1e-28) rinv = 1e14;
+  return rinv * kInv4Pi;
+}
+__device__ __forceinline__ cd green_c(double r2, const KParams& kp) {
+  double r = sqrt(r2);
+  r = fmax(r, 1e-14);
+  double s, c;
+  sincos(kp.kr * r, &s, &c);
+  double a = kInv4Pi / r;
+  if (kp.ki != 0.0) a *= exp(kp.ki * r);
+  return mk(a * c, -a * s);
+}
+template <class KT>
+__device__ __forceinline__ typename KT::S green_k(double r2, const KParams& kp) {
+  if constexpr (KT::KIND == 0)
+    return green(r2, kp, 0.0);
+  else
+    return green_c(r2, kp);
+}
+
+// -------------------------------------------------------- geometry jet
+// cf: [c][j][i] (stride 5 / 25), homogeneous (wx, wy, wz, w) in (s, t)
+template <int D>
+__device__ __forceinline__ void jet(const double* __restrict__ cf, double s, double t, double x[3],
+                                    double du[3], double dv[3]) {
+  double N[4], Ns[4], Nt[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* p = cf + c * 25;
+    double n = 0.0, ns = 0.0, nt = 0.0;
+#pragma unroll
+    for (int j = D; j >= 0; --j) {
+      double r = p[j * 5 + D], rp = 0.0;
+#pragma unroll
+      for (int i = D - 1; i >= 0; --i) {
+        rp = fma(rp, s, r);
+        r = fma(r, s, p[j * 5 + i]);
+      }
+      nt = fma(nt, t, n);
+      n = fma(n, t, r);
+      ns = fma(ns, t, rp);
+    }
+    N[c] = n;
+    Ns[c] = ns;
+    Nt[c] = nt;
+  }
+  const double iw = 1.0 / N[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    x[k] = N[k] * iw;
+    du[k] = (Ns[k] - x[k] * Ns[3]) * iw;
+    dv[k] = (Nt[k] - x[k] * Nt[3]) * iw;
+  }
+}
+template <int D>
+__device__ __forceinline__ void point_only(const double* __restrict__ cf, double s, double t, double x[3]) {
+  double N[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* p = cf + c * 25;
+    double n = 0.0;
+#pragma unroll
+    for (int j = D; j >= 0; --j) {
+      double r = p[j * 5 + D];
+#pragma unroll
+      for (int i = D - 1; i >= 0; --i) r = fma(r, s, p[j * 5 + i]);
+      n = fma(n, t, r);
+    }
+    N[c] = n;
+  }
+  const double iw = 1.0 / N[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) x[k] = N[k] * iw;
+}
+__device__ __forceinline__ double sqrt_g_of(const double du[3], const double dv[3]) {
+  const double n0 = du[1] * dv[2] - du[2] * dv[1];
+  const double n1 = du[2] * dv[0] - du[0] * dv[2];
+  const double n2 = du[0] * dv[1] - du[1] * dv[0];
+  return sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+}
+
+// polynomial of degree DEG with coefficients c[0..DEG]
+template <int DEG>
+__device__ __forceinline__ double horner(const double* c, double s) {
+  double r = c[DEG];
+#pragma unroll
+  for (int k = DEG - 1; k >= 0; --k) r = fma(r, s, c[k]);
+  return r;
+}
+template <int DEG>
+__device__ __forceinline__ double horner_d(const double* c, double s) {
+  if constexpr (DEG == 0) {
+    return 0.0;
+  } else {
+    double r = DEG * c[DEG];
+#pragma unroll
+    for (int k = DEG - 1; k >= 1; --k) r = fma(r, s, k * c[k]);
+    return r;
+  }
+}
+
+// shape data of one point: NC channels x NL values (real).
+// scalar: value; Maxwell: field x/y/z and surface divergence
+// (spaces.cpp:257-307).  tab: element tables in smem.
+template <class KT>
+__device__ __forceinline__ void shapes(const double* __restrict__ tab, double s, double t, double h,
+                                       const double du[3], const double dv[3], double sg,
+                                       double out[KT::NC][KT::NL]) {
+  if constexpr (KT::KIND != 2) {
+    constexpr int Q = KT::Q;
+    double bu[Q + 1], bv[Q + 1];
+#pragma unroll
+    for (int i = 0; i <= Q; ++i) {
+      bu[i] = horner<Q>(tab + i * (Q + 1), s);
+      bv[i] = horner<Q>(tab + (Q + 1) * (Q + 1) + i * (Q + 1), t);
+    }
+#pragma unroll
+    for (int j = 0; j <= Q; ++j)
+#pragma unroll
+      for (int i = 0; i <= Q; ++i) out[0][i + (Q + 1) * j] = bu[i] * bv[j];
+  } else {
+    constexpr int P = KT::Q;
+    const double* tpu = tab;
+    const double* tpv = tab + (P + 1) * (P + 1);
+    const double* tqu = tab + 2 * (P + 1) * (P + 1);
+    const double* tqv = tqu + P * P;
+    double bpu[P + 1], bpv[P + 1], dpu[P + 1], dpv[P + 1], bqu[P], bqv[P];
+    const double ih = 1.0 / h;
+#pragma unroll
+    for (int i = 0; i <= P; ++i) {
+      bpu[i] = horner<P>(tpu + i * (P + 1), s);
+      bpv[i] = horner<P>(tpv + i * (P + 1), t);
+      dpu[i] = horner_d<P>(tpu + i * (P + 1), s) * ih;
+      dpv[i] = horner_d<P>(tpv + i * (P + 1), t) * ih;
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      bqu[i] = horner<P - 1>(tqu + i * P, s);
+      bqv[i] = horner<P - 1>(tqv + i * P, t);
+    }
+    const double ig = 1.0 / sg;
+    int l = 0;
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+#pragma unroll
+      for (int i = 0; i <= P; ++i, ++l) {
+        const double b = bpu[i] * bqv[j];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) out[k][l] = ig * du[k] * b;
+        out[3][l] = ig * dpu[i] * bqv[j];
+      }
+#pragma unroll
+    for (int j = 0; j <= P; ++j)
+#pragma unroll
+      for (int i = 0; i < P; ++i, ++l) {
+        const double b = bqu[i] * bpv[j];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) out[k][l] = ig * dv[k] * b;
+        out[3][l] = ig * bqu[i] * dpv[j];
+      }
+  }
+}
+
+// element tables (u, v) for grid position (ix, iy) into smem
+template <class KT>
+__device__ __forceinline__ void load_tables(double* dst, const double* __restrict__ ta,
+                                            const double* __restrict__ tb, int ix, int iy, int tid,
+                                            int nthreads) {
+  if constexpr (KT::KIND != 2) {
+    constexpr int T = (KT::Q + 1) * (KT::Q + 1);
+    for (int i = tid; i < 2 * T; i += nthreads) dst[i] = (i < T) ? ta[ix * T + i] : ta[iy * T + i - T];
+  } else {
+    constexpr int P = KT::Q, TP = (P + 1) * (P + 1), TQ = P * P;
+    for (int i = tid; i < 2 * TP + 2 * TQ; i += nthreads) {
+      double v;
+      if (i < TP) v = ta[ix * TP + i];
+      else if (i < 2 * TP) v = ta[iy * TP + i - TP];
+      else if (i < 2 * TP + TQ) v = tb[ix * TQ + i - 2 * TP];
+      else v = tb[iy * TQ + i - 2 * TP - TQ];
+      dst[i] = v;
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace igb

@@ -62,6 +62,15 @@ class _Times(ctypes.Structure):
                                                "vertex_ms", "device_total_ms", "wall_total_ms")]
 
 
+class _SolverOpts(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int), ("restart", ctypes.c_int)]
+
+
+class _SolveStats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("residual", ctypes.c_double), ("converged", ctypes.c_int),
+                ("seconds", ctypes.c_double)]
+
+
 class _PatchDesc(ctypes.Structure):
     _fields_ = [("degree_u", ctypes.c_int), ("degree_v", ctypes.c_int), ("n_knots_u", ctypes.c_int),
                 ("n_knots_v", ctypes.c_int), ("knots_u", ctypes.POINTER(ctypes.c_double)),
@@ -77,6 +86,7 @@ SYMBOLS = (
     "igb_h2_dim", "igb_h2_apply", "igb_h2_apply_device", "igb_h2_storage_report", "igb_h2_counts",
     "igb_h2_near_pairs", "igb_h2_far_pairs", "igb_h2_tree", "igb_h2_near_blocks", "igb_h2_couplings",
     "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
+    "igb_h2_gmres", "igb_h2_cg", "igb_rhs_points", "igb_rhs_assemble", "igb_potential",
     "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_counts", "igb_plan_near_pairs",
     "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
@@ -148,6 +158,11 @@ def lib():
     L.igb_plan_owned.argtypes = [vp, i32, i32, P(ctypes.c_ubyte), P(ctypes.c_ubyte)]
     L.igb_plan_destroy.argtypes = [vp]
     L.igb_plan_destroy.restype = None
+    L.igb_h2_gmres.argtypes = [vp, P(f64), P(f64), P(_SolverOpts), P(_SolveStats)]
+    L.igb_h2_cg.argtypes = [vp, P(f64), P(f64), P(_SolverOpts), P(_SolveStats)]
+    L.igb_rhs_points.argtypes = [vp, i32, i32, P(f64), P(i32)]
+    L.igb_rhs_assemble.argtypes = [vp, i32, i32, P(f64), P(f64)]
+    L.igb_potential.argtypes = [vp, P(f64), i32, P(f64), i32, i32, P(f64)]
     L.igb_admissible.argtypes = [P(f64), P(f64), f64]
     L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
     _LIB = L
@@ -597,3 +612,99 @@ class DistH2Matrix:
         self.h.dist_phase2(self.recv.data_ptr(), y.data_ptr(), torch.cuda.current_stream().cuda_stream)
         self.dist.all_reduce(y, group=self.group)
         return y
+
+
+# ----------------------------------------------------------- SURVEY 8(f)
+@dataclass
+class SolverOptions:
+    """SolverOptions{tol = 1e-8, max_iter = 1000, restart = 30} (solver.hpp:37-41)."""
+    tol: float = 1e-8
+    max_iter: int = 1000
+    restart: int = 30
+
+
+@dataclass
+class SolveStats:
+    iterations: int
+    residual: float
+    converged: bool
+    seconds: float
+
+
+def _solve(fn, h, b, opts):
+    opts = opts or SolverOptions()
+    b = np.ascontiguousarray(b, dtype=h.dtype)
+    if b.shape != (h.rows(),):
+        raise ValueError("solver: dimension mismatch")
+    x = np.zeros_like(b)
+    st = _SolveStats()
+    o = _SolverOpts(float(opts.tol), int(opts.max_iter), int(opts.restart))
+    _check(fn(h._h, _p(b.view(np.float64)), _p(x.view(np.float64)), ctypes.byref(o), ctypes.byref(st)))
+    return x, SolveStats(st.iterations, st.residual, bool(st.converged), st.seconds)
+
+
+def gmres(h: H2Matrix, b, opts: SolverOptions | None = None):
+    """Restarted GMRES of solver.hpp:54-155 on the B200 operator; vectors stay in HBM."""
+    return _solve(lib().igb_h2_gmres, h, b, opts)
+
+
+def cg(h: H2Matrix, b, opts: SolverOptions | None = None):
+    """CG of solver.hpp:159-200 on the B200 operator."""
+    return _solve(lib().igb_h2_cg, h, b, opts)
+
+
+def quadrature_points(disc: Discretization, quad_order=0, device=0):
+    """Load-vector quadrature points, shape (elements, n^2, 3) (assembly.cpp:60-72)."""
+    npe = ctypes.c_int()
+    _check(lib().igb_rhs_points(disc._h, int(quad_order), int(device), None, ctypes.byref(npe)))
+    out = np.zeros((disc.element_count(), npe.value, 3))
+    _check(lib().igb_rhs_points(disc._h, int(quad_order), int(device), _p(out), ctypes.byref(npe)))
+    return out
+
+
+def compute_rhs(disc: Discretization, g, quad_order=0, device=0):
+    """b_i = <g, phi_i> (compute_rhs / compute_rhs_complex / compute_rhs_maxwell,
+    assembly.hpp:32-41).  g maps an (n, 3) array of points to n values
+    (Maxwell: an (n, 3) array of complex field vectors)."""
+    pts = quadrature_points(disc, quad_order, device)
+    vals = np.asarray(g(pts.reshape(-1, 3)))
+    pde = disc.pde()
+    dt = np.complex128 if pde.is_complex() else np.float64
+    if pde.is_vector():
+        vals = np.ascontiguousarray(vals, dtype=np.complex128).reshape(-1, 3)
+    else:
+        vals = np.ascontiguousarray(vals, dtype=dt).reshape(-1)
+    b = np.zeros(disc.dof_count(), dtype=dt)
+    _check(lib().igb_rhs_assemble(disc._h, int(quad_order), int(device), _p(vals.view(np.float64)),
+                                  _p(b.view(np.float64))))
+    return b
+
+
+def eval_potential(disc: Discretization, density, points, quad_order=10, device=0):
+    """Single layer potential at points (operators.hpp:44-49); Maxwell: the
+    electric field E = SL[j] + kappa^-2 grad SL[div j], shape (n, 3)."""
+    pde = disc.pde()
+    dt = np.complex128 if pde.is_complex() else np.float64
+    dens = np.ascontiguousarray(density, dtype=dt)
+    if dens.shape != (disc.dof_count(),):
+        raise ValueError("eval_potential: density size does not match the space")
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros((len(pts), 3) if pde.is_vector() else len(pts), dtype=dt)
+    _check(lib().igb_potential(disc._h, _p(dens.view(np.float64)), len(pts), _p(pts), int(quad_order), int(device),
+                               _p(out.view(np.float64))))
+    return out
+
+
+eval_maxwell_potential = eval_potential
+
+
+def make_sphere_grid(radius, n, center=(0.0, 0.0, 0.0)):
+    """util.cpp:9-24: n x n points on a sphere (theta-major)."""
+    if radius <= 0 or n < 1:
+        raise ValueError("make_sphere_grid: bad arguments")
+    k = np.arange(n)
+    theta = np.pi * (k + 0.5) / n
+    phi = 2.0 * np.pi * k / n
+    th, ph = np.meshgrid(theta, phi, indexing="ij")
+    pts = np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)], axis=-1).reshape(-1, 3)
+    return np.asarray(center, dtype=np.float64) + radius * pts

@@ -1,0 +1,114 @@
+"""SURVEY 8(f) on the B200 against the reference itself (oracle/_ref): load
+vectors, device-resident GMRES / CG (solver.hpp, same algorithm), potentials
+and the point-charge / dipole errors against analytic fields.  North star:
+solutions within 1e-8 relative, the same error against the analytic field."""
+import numpy as np
+import pytest
+
+from oracle import pyref
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not pyref.available(), reason="oracle/_ref not built")]
+
+X0 = np.array([0.0, 0.1, 1.5])
+
+
+def laplace_ps(p, x0=X0):
+    return 1.0 / (4 * np.pi * np.linalg.norm(p - x0, axis=1))
+
+
+def helmholtz_ps(p, k, x0=X0):
+    r = np.linalg.norm(p - x0, axis=1)
+    return np.exp(-1j * k * r) / (4 * np.pi * r)
+
+
+def maxwell_dipole(x, y0, pol, k):  # operators.cpp:7-20
+    d = x - y0
+    r = np.linalg.norm(d, axis=1)[:, None]
+    rhat = d / r
+    g = np.exp(-1j * k * r) / (4 * np.pi * r)
+    a = -1j * k - 1.0 / r
+    gp = g * a
+    gpp = g * (a * a + 1.0 / (r * r))
+    rp = (rhat @ pol)[:, None]
+    return k * k * g * pol + (gpp - gp / r) * rp * rhat + (gp / r) * pol
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_laplace_c1_pipeline(igb):
+    """c1: point charge, CG and GMRES on the H2 operator, interior potential error"""
+    d = igb.Discretization(igb.make_sphere(), igb.Pde.laplace(), 2, 1, 3)
+    h = igb.H2Matrix(d, igb.H2Options(m=8))
+    rd = pyref.Discretization("laplace", 2, 1, 3)
+    rh = pyref.H2Matrix(rd, m=8)
+    b = igb.compute_rhs(d, laplace_ps)
+    rb = rd.rhs(0, X0)
+    assert _rel(b, rb) < 1e-13
+    grid = igb.make_sphere_grid(0.5, 10)  # tools/main.cpp:218-220 interior default
+    exact = laplace_ps(grid)
+    # GMRES (the CLI's solver, restart 200) tracks the reference iterate for
+    # iterate at tol 1e-8.  CG is rounding-sensitive (loss of orthogonality):
+    # two runs that both meet tol 1e-8 differ by ~cond * tol, so its solution
+    # parity is checked at tol 1e-12 (measured: 72 vs 75 its / 5.6e-7 at 1e-8;
+    # 128 vs 130 its / 2e-11 at 1e-12).
+    for method, opts, its in (("gmres", igb.SolverOptions(tol=1e-8, max_iter=5000, restart=200), 1),
+                              ("cg", igb.SolverOptions(tol=1e-12, max_iter=5000), 3)):
+        fn = igb.cg if method == "cg" else igb.gmres
+        x, st = fn(h, b, opts)
+        rx, rst = rh.solve(rb, method, tol=opts.tol, max_iter=opts.max_iter, restart=opts.restart)
+        assert st.converged and rst["converged"]
+        assert abs(st.iterations - rst["iterations"]) <= its
+        assert _rel(x, rx) < 1e-8  # north star: GMRES/CG solution within 1e-8
+        u = igb.eval_potential(d, x, grid)
+        ru = rd.potential(rx, grid)
+        assert _rel(u, ru) < 1e-10
+        err, rerr = np.abs(u - exact).max(), np.abs(ru - exact).max()
+        assert abs(err - rerr) <= 1e-3 * rerr  # same point-charge error
+        assert err < 1e-5
+
+
+def test_helmholtz_pipeline(igb):
+    k = 3.0
+    d = igb.Discretization(igb.make_sphere(), igb.Pde.helmholtz(k), 2, 1, 2)
+    h = igb.H2Matrix(d, igb.H2Options(m=8))
+    rd = pyref.Discretization("helmholtz", 2, 1, 2, kappa=k)
+    rh = pyref.H2Matrix(rd, m=8)
+    b = igb.compute_rhs(d, lambda p: helmholtz_ps(p, k))
+    rb = rd.rhs(1, X0)
+    assert _rel(b, rb) < 1e-13
+    opts = igb.SolverOptions(tol=1e-10, max_iter=2000, restart=50)
+    x, st = igb.gmres(h, b, opts)
+    rx, rst = rh.solve(rb, "gmres", tol=opts.tol, max_iter=opts.max_iter, restart=opts.restart)
+    assert st.converged and abs(st.iterations - rst["iterations"]) <= 1
+    assert _rel(x, rx) < 1e-8
+    grid = igb.make_sphere_grid(0.5, 6)
+    assert _rel(igb.eval_potential(d, x, grid), rd.potential(rx, grid)) < 1e-10
+
+
+def test_maxwell_dipole_and_plane_wave(igb):
+    k = 2 * np.pi
+    d = igb.Discretization(igb.make_sphere(), igb.Pde.maxwell(k), 2, 1, 2)
+    h = igb.H2Matrix(d, igb.H2Options(m=6))
+    rd = pyref.Discretization("maxwell", 2, 1, 2, kappa=k)
+    rh = pyref.H2Matrix(rd, m=6)
+    y0, pol = np.array([0.0, 0.0, 0.3]), np.array([1.0, 0.0, 0.0])
+    b = igb.compute_rhs(d, lambda p: maxwell_dipole(p, y0, pol, k))
+    assert _rel(b, rd.rhs(2, np.r_[y0, pol])) < 1e-13
+    # c4 excitation: plane wave along z, polarisation x (E = -pol e^{-i k z})
+    bw = igb.compute_rhs(d, lambda p: -pol[None, :] * np.exp(-1j * k * p[:, 2:3]))
+    rbw = rd.rhs(3, [0, 0, 1, 1, 0, 0])
+    assert _rel(bw, rbw) < 1e-13
+    # the EFIE is ill-conditioned: at tol 1e-8 two valid GMRES(50) runs differ
+    # by ~5e-8 (632 vs 636 its); at tol 1e-10, restart 200 (the CLI's) the
+    # iterations match (143 = 143) and the solutions agree to ~5e-11
+    opts = igb.SolverOptions(tol=1e-10, max_iter=3000, restart=200)
+    x, st = igb.gmres(h, bw, opts)
+    rx, rst = rh.solve(rbw, "gmres", tol=opts.tol, max_iter=opts.max_iter, restart=opts.restart)
+    assert st.converged and abs(st.iterations - rst["iterations"]) <= 2
+    assert _rel(x, rx) < 1e-8
+    g = np.random.default_rng(20261019).standard_normal((100, 3))
+    pts = 3.0 * g / np.linalg.norm(g, axis=1)[:, None]  # c4: 100 seeded points on radius 3
+    e, re = igb.eval_maxwell_potential(d, x, pts), rd.potential(rx, pts)
+    assert _rel(e, re) < 1e-10
