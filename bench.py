@@ -41,6 +41,15 @@ CONFIGS = {
 FP64_PEAK_TFLOPS = 36.85  # DFMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak_probe.txt)
 
 
+def load_traffic():
+    """per-launch DRAM bytes of the dominant kernels from the committed ncu capture"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic_c2.json")) as f:
+            return json.load(f)["kernels"]
+    except Exception:
+        return {}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -242,26 +251,49 @@ def run_b200(args, c, name):
     for k, v in prof.items():
         kernels["matvec_" + k] = v * mv
     dominant = max(kernels, key=kernels.get)
-    far_bytes = far_kernel_bytes(h, c)
-    far_ms = prof["far"]
     sing_pts = singular_points(h, c)
     n_asm_k, n_mv_k = h.launch_counts()
     launches = args.steps * (n_asm_k + mv * n_mv_k)
-    rooflines = {
-        "matvec_far": {"bound": "hbm", "achieved": far_bytes / (far_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                       "peak_source": src, "traffic": None, "bytes_per_launch": far_bytes, "ms": far_ms},
-    }
+    traffic = load_traffic()
+    mm = c["m"] ** 2
+    fp64 = FP64_PEAK_TFLOPS
+    rooflines = {}
+    far_ms = prof["far"]
+    if h.stored_couplings:
+        fb = far_kernel_bytes(h, c)
+        rooflines["matvec_far"] = {"bound": "hbm", "achieved": fb / (far_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                   "peak_source": src, "bytes_per_launch": fb, "ms": far_ms}
+    else:
+        sym = c["kind"] == "laplace" and 2 <= c["m"] <= 6
+        evals = (h.far_count // 2 if sym else h.far_count) * mm * mm
+        fl = evals * (20 if sym else 19) * (1 if h.dtype == np.float64 else 4)
+        rooflines["matvec_far"] = {"bound": "fp64", "achieved": fl / (far_ms * 1e-3) / 1e12, "peak": fp64,
+                                   "unit": "TFLOP/s", "peak_source": "measured DFMA probe (profiles/r01_fp64_peak_probe.txt)",
+                                   "flops_per_launch": fl, "kernel_evals": evals, "ms": far_ms,
+                                   "note": "couplings evaluated on the fly (symmetric: each unordered pair once)"
+                                   if sym else "couplings evaluated on the fly"}
+        kt = traffic.get(f"k_far_sym<{c['m']}>")
+        if kt:
+            rooflines["matvec_far"]["traffic"] = kt["dram_read_bytes"] + kt["dram_write_bytes"]
+    nb = h.device_bytes()["near"]
+    rooflines["matvec_near"] = {"bound": "hbm", "achieved": nb / (prof["near_leaf"] * 1e-3) / 1e9, "peak": hbm,
+                                "unit": "GB/s", "peak_source": src, "bytes_per_launch": nb, "ms": prof["near_leaf"],
+                                "note": "near rows + leaf backward, timed serialised (overlapped in the graph)"}
+    kt = traffic.get(f"k_near_rows<double, {disc.local_count()}>")
+    if kt:
+        rooflines["matvec_near"]["traffic"] = kt["dram_read_bytes"] + kt["dram_write_bytes"]
     for cls, key in (("edge", "edge_ms"), ("vertex", "vertex_ms"), ("coincident", "coincident_ms")):
         fl = sing_pts[cls] * flops_per_point(c, disc)
         ms = times[key]
         if ms > 0:
-            rooflines["singular_" + cls] = {"bound": "fp64", "achieved": fl / (ms * 1e-3) / 1e12,
-                                           "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                           "peak_source": "measured DFMA probe", "traffic": None,
+            rooflines["singular_" + cls] = {"bound": "fp64", "achieved": fl / (ms * 1e-3) / 1e12, "peak": fp64,
+                                           "unit": "TFLOP/s", "peak_source": "measured DFMA probe",
                                            "flops_per_launch": fl, "ms": ms, "points": sing_pts[cls]}
     for r in rooflines.values():
         r["frac"] = r["achieved"] / r["peak"]
-    dom_key = "matvec_far" if dominant == "matvec_far" else (dominant if dominant in rooflines else "matvec_far")
+        r.setdefault("traffic", None)
+    dom_key = {"matvec_far": "matvec_far", "matvec_near_leaf": "matvec_near", "singular_edge": "singular_edge",
+               "singular_vertex": "singular_vertex", "singular_coincident": "singular_coincident"}.get(dominant, "matvec_far")
     roof = {k: rooflines[dom_key][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
     roof["kernel"] = dom_key
     # -- e2e through the public API with host buffers
@@ -292,7 +324,7 @@ def run_b200(args, c, name):
     out = None
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu:
+        if world == 1 and not args.no_cpu and name in ("c1", "c2", "c4"):  # c3 / c5: CPU operator does not fit host RAM
             os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
             info = cpu_sample(c)
             cpu = {"value": mv * info["dofs"] / info["step_s"] / 1e9, "unit": "GDOF/s", "cores": info["cores"],

@@ -1,7 +1,7 @@
 #!/bin/bash
-# bench + launch list + one full ncu capture of the top kernels (run under gpurun)
+# default bench run (as the driver runs it) + smoke
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-tail -3 gpurun_out/bench.log
-cat gpurun_out/smoke.log
+python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+cat gpurun_out/smoke.log; tail -2 gpurun_out/bench.log | cut -c1-600; tail -2 gpurun_out/bench_ref.log | cut -c1-900
