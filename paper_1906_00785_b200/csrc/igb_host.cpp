@@ -5,7 +5,12 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <omp.h>
+
 #include <parallel/algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 namespace igb {
 
@@ -970,6 +975,14 @@ void lagrange_all(const std::vector<double>& nodes, double x, double* out) {  //
 
 // ------------------------------------------------------------ H2 plan
 H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order) {
+  static const bool verbose = getenv("IGB_VERBOSE") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!verbose) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[igb plan] %-14s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   if (m < 2) throw std::invalid_argument("H2Matrix: interpolation degree m < 2");
   if (!(eta > 0)) throw std::invalid_argument("H2Matrix: eta must be positive");
   H2Plan P;
@@ -1014,86 +1027,140 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
           }
         }
     }
-  // dual traversal (h2.cpp:198-216), parallel over root pairs
+  lap("tree");
+  // dual traversal (h2.cpp:198-216).  Same-level recursion from every ordered
+  // root pair; decided pairs of levels 0-1 are collected serially and the
+  // undecided level-2 pairs are traversed in parallel (balanced work list).
   std::vector<double> diag(nn);
   for (int i = 0; i < nn; ++i) diag[i] = P.node_box[i].diag_norm();
-  std::vector<std::vector<uint64_t>> far_parts(np * np), near_parts(np * np);
-#pragma omp parallel for schedule(dynamic)
-  for (int rp = 0; rp < np * np; ++rp) {
-    auto& fo = far_parts[rp];
-    auto& no = near_parts[rp];
-    auto traverse = [&](auto&& self, int a, int b) -> void {
-      const double dist = P.node_box[a].exterior_distance(P.node_box[b]);
-      if (std::max(diag[a], diag[b]) <= eta * dist) {  // h2.cpp:92-97
-        fo.push_back((static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b));
-        return;
+  auto child = [&](int node, int k) {
+    return static_cast<int>(P.node_id(P.node_patch[node], P.node_level[node] + 1, 2 * P.node_sx[node] + (k & 1),
+                                      2 * P.node_sy[node] + (k >> 1)));
+  };
+  auto leaf_el = [&](int node) { return d.element_index(P.node_patch[node], P.node_sx[node], P.node_sy[node]); };
+  // returns 0 far, 1 near (leaf), 2 recurse
+  auto decide = [&](int a, int b) {
+    const double dist = P.node_box[a].exterior_distance(P.node_box[b]);
+    if (std::max(diag[a], diag[b]) <= eta * dist) return 0;  // h2.cpp:92-97
+    return P.node_level[a] == L ? 1 : 2;
+  };
+  std::vector<std::pair<int, int>> far_top, near_top, work;
+  {
+    std::vector<std::pair<int, int>> cur;
+    for (int pa = 0; pa < np; ++pa)
+      for (int pb = 0; pb < np; ++pb)
+        cur.emplace_back(static_cast<int>(P.node_id(pa, 0, 0, 0)), static_cast<int>(P.node_id(pb, 0, 0, 0)));
+    for (int lev = 0; lev < 2 && !cur.empty(); ++lev) {
+      std::vector<std::pair<int, int>> nxt;
+      for (auto [a, b] : cur) {
+        const int c = decide(a, b);
+        if (c == 0) far_top.emplace_back(a, b);
+        else if (c == 1) near_top.emplace_back(leaf_el(a), leaf_el(b));
+        else
+          for (int ka = 0; ka < 4; ++ka)
+            for (int kb = 0; kb < 4; ++kb) nxt.emplace_back(child(a, ka), child(b, kb));
       }
-      if (P.node_level[a] == L) {
-        const int ea = d.element_index(P.node_patch[a], P.node_sx[a], P.node_sy[a]);
-        const int eb = d.element_index(P.node_patch[b], P.node_sx[b], P.node_sy[b]);
-        no.push_back((static_cast<uint64_t>(ea) << 32) | static_cast<uint32_t>(eb));
-        return;
-      }
-      const int la = P.node_level[a] + 1, lb = P.node_level[b] + 1;
-      for (int ka = 0; ka < 4; ++ka)
-        for (int kb = 0; kb < 4; ++kb)
-          self(self,
-               static_cast<int>(P.node_id(P.node_patch[a], la, 2 * P.node_sx[a] + (ka & 1), 2 * P.node_sy[a] + (ka >> 1))),
-               static_cast<int>(P.node_id(P.node_patch[b], lb, 2 * P.node_sx[b] + (kb & 1), 2 * P.node_sy[b] + (kb >> 1))));
-    };
-    traverse(traverse, static_cast<int>(P.node_id(rp / np, 0, 0, 0)), static_cast<int>(P.node_id(rp % np, 0, 0, 0)));
-  }
-  auto gather = [&](std::vector<std::vector<uint64_t>>& parts, std::vector<int>& A, std::vector<int>& B) {
-    size_t tot = 0;
-    for (auto& p : parts) tot += p.size();
-    std::vector<uint64_t> keys;
-    keys.reserve(tot);
-    for (auto& p : parts) {
-      keys.insert(keys.end(), p.begin(), p.end());
-      std::vector<uint64_t>().swap(p);
+      cur.swap(nxt);
     }
-    __gnu_parallel::sort(keys.begin(), keys.end());
+    work.swap(cur);
+  }
+  const int nw = static_cast<int>(work.size());
+  std::vector<std::vector<std::pair<int, int>>> far_parts(nw + 1), near_parts(nw + 1);
+  far_parts[nw] = std::move(far_top);
+  near_parts[nw] = std::move(near_top);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int w = 0; w < nw; ++w) {
+    auto& fo = far_parts[w];
+    auto& no = near_parts[w];
+    auto traverse = [&](auto&& self, int a, int b) -> void {
+      const int c = decide(a, b);
+      if (c == 0) {
+        fo.emplace_back(a, b);
+        return;
+      }
+      if (c == 1) {
+        no.emplace_back(leaf_el(a), leaf_el(b));
+        return;
+      }
+      for (int ka = 0; ka < 4; ++ka)
+        for (int kb = 0; kb < 4; ++kb) self(self, child(a, ka), child(b, kb));
+    };
+    traverse(traverse, work[w].first, work[w].second);
+  }
+  lap("traversal");
+  // counting sort by row with per-thread histograms (stable, parallel), then
+  // each short row by column: the lexicographic order of h2.cpp:215-216 and
+  // the CSR row starts of h2.cpp:245-251
+  auto bucket = [&](std::vector<std::vector<std::pair<int, int>>>& parts, int nrows, std::vector<int>& A,
+                    std::vector<int>& B, std::vector<int>& rs) {
+    const int nparts = static_cast<int>(parts.size());
+    long long tot = 0;
+    for (const auto& v : parts) tot += static_cast<long long>(v.size());
+    if (tot > 0x7fffffffLL) throw std::runtime_error("B200 H2: too many block pairs for 32-bit indexing");
+    const int T = std::max(1, std::min(omp_get_max_threads(), nparts));
+    std::vector<std::vector<int>> hist(T, std::vector<int>(nrows, 0));
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int t = 0; t < T; ++t)
+      for (int i = static_cast<int>(static_cast<long long>(nparts) * t / T);
+           i < static_cast<int>(static_cast<long long>(nparts) * (t + 1) / T); ++i)
+        for (const auto& pr : parts[i]) ++hist[t][pr.first];
+    rs.assign(nrows + 1, 0);
+    {
+      int run = 0;
+      for (int r = 0; r < nrows; ++r) {
+        rs[r] = run;
+        for (int t = 0; t < T; ++t) {
+          const int c = hist[t][r];
+          hist[t][r] = run;
+          run += c;
+        }
+      }
+      rs[nrows] = run;
+    }
+    B.assign(tot, 0);
     A.resize(tot);
-    B.resize(tot);
-#pragma omp parallel for schedule(static)
-    for (long long i = 0; i < static_cast<long long>(tot); ++i) {
-      A[i] = static_cast<int>(keys[i] >> 32);
-      B[i] = static_cast<int>(keys[i] & 0xffffffffu);
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int t = 0; t < T; ++t)
+      for (int i = static_cast<int>(static_cast<long long>(nparts) * t / T);
+           i < static_cast<int>(static_cast<long long>(nparts) * (t + 1) / T); ++i) {
+        for (const auto& pr : parts[i]) B[hist[t][pr.first]++] = pr.second;
+        std::vector<std::pair<int, int>>().swap(parts[i]);
+      }
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int r = 0; r < nrows; ++r) {
+      std::sort(B.begin() + rs[r], B.begin() + rs[r + 1]);
+      for (int q = rs[r]; q < rs[r + 1]; ++q) A[q] = r;
     }
   };
-  gather(far_parts, P.far_a, P.far_b);
-  gather(near_parts, P.near_a, P.near_b);
+  bucket(far_parts, nn, P.far_a, P.far_b, P.far_row_start);
+  bucket(near_parts, ne, P.near_a, P.near_b, P.near_row_start);
+  lap("sort");
   const long long nnear = static_cast<long long>(P.near_a.size());
   const long long nfar_pairs = static_cast<long long>(P.far_a.size());
-  if (nfar_pairs > 0x7fffffffLL || nnear > 0x7fffffffLL)
-    throw std::runtime_error("B200 H2: too many block pairs for 32-bit indexing");
-  P.near_row_start.assign(ne + 1, 0);
-  for (long long q = 0; q < nnear; ++q) ++P.near_row_start[P.near_a[q] + 1];
-  for (int e = 0; e < ne; ++e) P.near_row_start[e + 1] += P.near_row_start[e];
-  P.far_row_start.assign(nn + 1, 0);
-  for (long long q = 0; q < nfar_pairs; ++q) ++P.far_row_start[P.far_a[q] + 1];
-  for (int t = 0; t < nn; ++t) P.far_row_start[t + 1] += P.far_row_start[t];
-  // symmetric structure of the admissible pairs: (t, s) <-> (s, t)
-  P.far_upper_start.resize(nn);
+  lap("row starts");
+  // symmetric structure of the admissible pairs: (t, s) <-> (s, t).  Pairs
+  // (s, t) enumerated row-major and bucketed stably by t arrive in (t, s) order,
+  // i.e. at the position of their transpose: an O(N) counting sort.
   P.far_trans.assign(nfar_pairs, -1);
+  {
+    std::vector<int> fillp(P.far_row_start.begin(), P.far_row_start.end() - 1);
+    for (long long q = 0; q < nfar_pairs; ++q) P.far_trans[fillp[P.far_b[q]]++] = static_cast<int>(q);
+    for (int t = 0; t < nn; ++t)
+      if (fillp[t] != P.far_row_start[t + 1]) throw std::logic_error("B200 H2: admissible relation is not symmetric");
+  }
+  P.far_upper_start.resize(nn);
   int asym = 0;
-#pragma omp parallel for schedule(dynamic, 256) reduction(+ : asym)
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : asym)
   for (int t = 0; t < nn; ++t) {
     const auto first = P.far_b.begin() + P.far_row_start[t], last = P.far_b.begin() + P.far_row_start[t + 1];
     P.far_upper_start[t] = static_cast<int>(std::upper_bound(first, last, t) - P.far_b.begin());
     for (int q = P.far_row_start[t]; q < P.far_row_start[t + 1]; ++q) {
-      const int s = P.far_b[q];
-      const auto f2 = P.far_b.begin() + P.far_row_start[s], l2 = P.far_b.begin() + P.far_row_start[s + 1];
-      const auto it = std::lower_bound(f2, l2, t);
-      if (it == l2 || *it != t) {
-        ++asym;
-        continue;
-      }
-      P.far_trans[q] = static_cast<int>(it - P.far_b.begin());
+      const int tq = P.far_trans[q];
+      if (P.far_a[tq] != P.far_b[q] || P.far_b[tq] != t) ++asym;
     }
   }
   if (asym) throw std::logic_error("B200 H2: admissible relation is not symmetric");
-
+  lap("transposes");
   // classification + unique singular work lists
   P.near_cls.resize(nnear);
   std::vector<uint8_t> mapa(nnear), mapb(nnear);
@@ -1109,25 +1176,53 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
     const auto first = P.near_b.begin() + P.near_row_start[ea];
     const auto last = P.near_b.begin() + P.near_row_start[ea + 1];
     const auto it = std::lower_bound(first, last, eb);
-    if (it == last || *it != eb) throw std::logic_error("B200 H2: near relation is not symmetric");
+    if (it == last || *it != eb) return -1;
     return static_cast<int>(it - P.near_b.begin());
   };
+  // unique singular work items (ea <= eb) per class and the regular slots, in
+  // near-list order: per-class prefix sums, then a parallel fill
+  std::vector<unsigned char> kind(nnear);  // 0 regular, 1..3 singular item, 4 skip (ea > eb singular)
+#pragma omp parallel for schedule(static)
   for (long long q = 0; q < nnear; ++q) {
-    const int ea = P.near_a[q], eb = P.near_b[q];
-    const int cls = P.near_cls[q];
-    if (cls == kFar) {
-      P.reg_slot.push_back(static_cast<int>(q));
+    const int c = P.near_cls[q];
+    kind[q] = c == kFar ? 0 : (P.near_a[q] > P.near_b[q] ? 4 : static_cast<unsigned char>(c));
+  }
+  std::vector<long long> pos(nnear);
+  long long counts[5] = {0, 0, 0, 0, 0};
+  for (long long q = 0; q < nnear; ++q) pos[q] = counts[kind[q]]++;
+  P.reg_slot.resize(counts[0]);
+  for (int c = 1; c <= 3; ++c) {
+    auto& L2 = P.sing[c];
+    L2.ea.resize(counts[c]);
+    L2.eb.resize(counts[c]);
+    L2.map_a.resize(counts[c]);
+    L2.map_b.resize(counts[c]);
+    L2.slot_ab.resize(counts[c]);
+    L2.slot_ba.resize(counts[c]);
+  }
+  int missing = 0;
+#pragma omp parallel for schedule(static) reduction(+ : missing)
+  for (long long q = 0; q < nnear; ++q) {
+    const int k = kind[q];
+    if (k == 4) continue;
+    if (k == 0) {
+      P.reg_slot[pos[q]] = static_cast<int>(q);
       continue;
     }
-    if (ea > eb) continue;
-    auto& L2 = P.sing[cls];
-    L2.ea.push_back(ea);
-    L2.eb.push_back(eb);
-    L2.map_a.push_back(mapa[q]);
-    L2.map_b.push_back(mapb[q]);
-    L2.slot_ab.push_back(static_cast<int>(q));
-    L2.slot_ba.push_back(ea == eb ? static_cast<int>(q) : find_slot(eb, ea));
+    const int ea = P.near_a[q], eb = P.near_b[q];
+    auto& L2 = P.sing[k];
+    const long long i = pos[q];
+    L2.ea[i] = ea;
+    L2.eb[i] = eb;
+    L2.map_a[i] = mapa[q];
+    L2.map_b[i] = mapb[q];
+    L2.slot_ab[i] = static_cast<int>(q);
+    const int sba = ea == eb ? static_cast<int>(q) : find_slot(eb, ea);
+    if (sba < 0) ++missing;
+    L2.slot_ba[i] = sba;
   }
+  if (missing) throw std::logic_error("B200 H2: near relation is not symmetric");
+  lap("classify");
   // DOF incidence in ascending (e, l) order (h2.cpp:359-376 scatter order)
   const int nl = d.local_count(), nd = d.dof_count();
   P.dof_start.assign(nd + 1, 0);
@@ -1140,6 +1235,7 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
       const int i = e * nl + l;
       P.dof_inc[fillp[d.l2g()[i]]++] = i;
     }
+  lap("dof incidence");
   // interpolation (h2.cpp:113-125)
   P.cheb = cheb_nodes(m);
   P.tl.assign(m * m, 0.0);
