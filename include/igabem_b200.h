@@ -149,7 +149,8 @@ int igb_h2_images(const igb_h2* h, double* out);
 /* ---- measurement ---- */
 typedef struct {
   double plan_host_ms, upload_ms, elements_ms, images_ms, couplings_ms, regular_ms, coincident_ms,
-      edge_ms, vertex_ms, device_total_ms, wall_total_ms;
+      edge_ms, vertex_ms, device_total_ms, wall_total_ms,
+      scatter_ms; /* singular blocks -> near slots (they are integrated before the partition exists) */
 } igb_h2_times;
 int igb_h2_assembly_times(const igb_h2* h, igb_h2_times* out);
 /* bytes of the device-resident operator in this implementation's format */
@@ -195,6 +196,11 @@ int igb_plan_partition(const igb_plan* p, int world, int rank, int* c0, int* c1,
 /* ownership masks of that rank: element_owned[ne], node_owned[n_nodes]
  * (roots are owned by every rank) */
 int igb_plan_owned(const igb_plan* p, int world, int rank, unsigned char* element_owned, unsigned char* node_owned);
+/* Singular items (class >= 1, ea <= eb) of rank `rank` enumerated from the mesh
+   topology alone (what the device integrates before the partition exists):
+   counts[c] per class, *mismatch = 1 unless they equal the near list's singular
+   pairs of build_local_plan (spaces.cpp:309-394 classes over h2.cpp:175-252). */
+int igb_plan_singular_items(const igb_plan* p, int world, int rank, long long counts[4], int* mismatch);
 void igb_plan_destroy(igb_plan* p);
 
 /* ---- around the operator ---- */

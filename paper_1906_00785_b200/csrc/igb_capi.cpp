@@ -365,6 +365,7 @@ int igb_h2_assembly_times(const igb_h2* h, igb_h2_times* o) {
     o->vertex_ms = t.singular[1];
     o->device_total_ms = t.total_device;
     o->wall_total_ms = t.total_wall;
+    o->scatter_ms = t.scatter;
   });
 }
 int igb_h2_device_bytes(const igb_h2* h, size_t* near, size_t* far, size_t* moments) {
@@ -511,6 +512,26 @@ int igb_plan_owned(const igb_plan* p, int world, int rank, unsigned char* elemen
     if (element_owned)
       for (size_t e = 0; e < lp.el_local.size(); ++e) element_owned[e] = lp.el_local[e] >= 0 ? 1 : 0;
     if (node_owned) std::copy(lp.node_owned.begin(), lp.node_owned.end(), node_owned);
+  });
+}
+int igb_plan_singular_items(const igb_plan* p, int world, int rank, long long counts[4], int* mismatch) {
+  return guard([&] {
+    need(p, "plan");
+    std::vector<unsigned char> own;
+    if (world > 1) own = igb::owned_elements(*p->d, world, rank);
+    igb::SingList items[4];
+    p->d->singular_items(own.empty() ? nullptr : own.data(), items);
+    const auto lp = igb::build_local_plan(*p->d, p->plan, world, rank);
+    int bad = 0;
+    for (int c = 1; c <= 3; ++c) {
+      const auto &T = items[c], &L = lp.sing[c];
+      bad |= T.ea != L.ea || T.eb != L.eb || T.map_a != L.map_a || T.map_b != L.map_b;
+    }
+    if (counts) {
+      counts[0] = static_cast<long long>(lp.reg_slot.size());
+      for (int c = 1; c <= 3; ++c) counts[c] = static_cast<long long>(items[c].ea.size());
+    }
+    if (mismatch) *mismatch = bad;
   });
 }
 void igb_plan_destroy(igb_plan* p) { delete p; }

@@ -14,6 +14,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -291,11 +293,10 @@ __device__ __forceinline__ void apply_map(int bits, double& u, double& v) {  // 
 
 struct SingArgs {
   int n_pairs, n;
-  const int *ea, *eb, *slot_ab, *slot_ba;
+  const int *ea, *eb;
   const unsigned char *map_a, *map_b;
   const double *gx, *gw;
-  const int *near_a, *near_rs;
-  double* near;
+  double* out;  // compact blocks [item][la][lb] (scattered by k_sing_scatter)
 };
 
 template <class KT>
@@ -438,14 +439,37 @@ __global__ void __launch_bounds__(128) k_singular(GeoArgs g, SingArgs A) {
       for (int j = 0; j < TS; ++j) red[(slice * NL + tr + i) * NL + tc + j] = acc[i][j];
   }
   __syncthreads();
-  S* out = reinterpret_cast<S*>(A.near);
-  const int qab = A.slot_ab[pr], qba = A.slot_ba[pr];
+  S* out = reinterpret_cast<S*>(A.out) + static_cast<size_t>(pr) * NL * NL;
   for (int o = tid; o < NL * NL; o += 128) {
     S v = zero<S>();
     for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + o];
+    out[o] = v;
+  }
+}
+
+// Singular blocks are integrated before the block partition exists (they only
+// need the mesh topology); once the near list is known each item's block goes
+// to the slot of (ea, eb) and its transpose to the slot of (eb, ea) (the
+// bilinear forms are symmetric: spaces.cpp singular pairs are computed once).
+template <class S, int NL>
+__global__ void __launch_bounds__(128) k_sing_scatter(const int* __restrict__ slot_ab, const int* __restrict__ slot_ba,
+                                                      const int* __restrict__ near_a, const int* __restrict__ near_rs,
+                                                      const S* __restrict__ blk, S* __restrict__ near) {
+  __shared__ S tr[NL][NL + 1];
+  const int k = blockIdx.x;
+  const S* b = blk + static_cast<size_t>(k) * NL * NL;
+  const int qab = slot_ab[k], qba = slot_ba[k];
+  for (int o = threadIdx.x; o < NL * NL; o += blockDim.x) {
     const int la = o / NL, lb = o % NL;
-    if (qab >= 0) out[near_off(A.near_a, A.near_rs, qab, la, lb, NL)] = v;
-    if (qba >= 0 && qba != qab) out[near_off(A.near_a, A.near_rs, qba, lb, la, NL)] = v;
+    const S v = b[o];
+    tr[la][lb] = v;
+    if (qab >= 0) near[near_off(near_a, near_rs, qab, la, lb, NL)] = v;
+  }
+  if (qba < 0 || qba == qab) return;  // block-uniform
+  __syncthreads();
+  for (int o = threadIdx.x; o < NL * NL; o += blockDim.x) {
+    const int r = o / NL, c = o % NL;
+    near[near_off(near_a, near_rs, qba, r, c, NL)] = tr[c][r];
   }
 }
 
@@ -995,19 +1019,89 @@ __global__ void k_zero(size_t n, S* p) {
 // ====================================================== host driver
 using namespace dev;
 
+// Device memory comes from one stream-ordered pool per device that keeps
+// freed memory reserved (release threshold = max): operators built and
+// destroyed repeatedly -- a solve per right-hand side / geometry -- reuse it
+// instead of paying the driver's map / unmap on every construction.
+static cudaMemPool_t device_pool(int device) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pools.find(device);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t pool;
+  IGB_CUDA(cudaMemPoolCreate(&pool, &props));
+  uint64_t keep = UINT64_MAX;
+  IGB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  pools[device] = pool;
+  return pool;
+}
+
+// Pinned host staging buffers of the host-vector apply, recycled across
+// operators (cudaMallocHost costs milliseconds).
+static std::mutex g_pinned_mu;
+static std::multimap<size_t, void*> g_pinned_free;
+static std::map<void*, size_t>& g_pinned_sizes() {
+  static std::map<void*, size_t> m;
+  return m;
+}
+static void pinned_put(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(g_pinned_mu);
+  g_pinned_free.emplace(g_pinned_sizes()[p], p);
+}
+static void* pinned_get(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lock(g_pinned_mu);
+    auto it = g_pinned_free.lower_bound(bytes);
+    if (it != g_pinned_free.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      g_pinned_free.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  IGB_CUDA(cudaMallocHost(&p, bytes));
+  std::lock_guard<std::mutex> lock(g_pinned_mu);
+  g_pinned_sizes()[p] = bytes;
+  return p;
+}
+
 template <class T>
 T* H2Device::dalloc(size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
-  IGB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t s = up_stream_ ? up_stream_ : stream_;
+  const cudaError_t e = cudaMallocFromPoolAsync(&p, n * sizeof(T), device_pool(device_), s);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw std::runtime_error("B200 H2: out of device memory (" + std::to_string(n * sizeof(T)) + " bytes)");
+  }
+  IGB_CUDA(e);
+  alloc_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   allocs_.push_back(p);
   return static_cast<T*>(p);
+}
+
+void H2Device::release_memory() {
+  // work on user streams (apply_device) may still read the buffers: the same
+  // device-wide wait cudaFree performs, then the stream-ordered frees
+  cudaDeviceSynchronize();
+  for (void* p : allocs_) cudaFreeAsync(p, stream_);
+  allocs_.clear();
+  cudaStreamSynchronize(stream_);
 }
 template <class T>
 T* H2Device::upload(const std::vector<T>& v) {
   T* p = dalloc<T>(v.size());
   upload_bytes_ += v.size() * sizeof(T);
-  if (!v.empty()) IGB_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream_));
+  if (!v.empty())
+    IGB_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, up_stream_ ? up_stream_ : stream_));
   return p;
 }
 
@@ -1019,50 +1113,31 @@ H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, i
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("H2Matrix: bad rank/world");
   if (world > 1 && (flags & 2)) throw std::invalid_argument("H2Matrix: stored couplings are single-GPU only");
   const auto t_wall0 = std::chrono::steady_clock::now();
+  check_h2_options(*disc_, m, eta, far_order, sing_order, &nfar_, &nsing_);
+  if (nsing_ > 16) throw std::invalid_argument("B200 H2: singular order > 16 not supported (32-bit point index)");
+  opt_ = {m, eta, far_order, sing_order, world, rank};
   int ndev = 0;
   IGB_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) throw std::invalid_argument("H2Matrix: CUDA device index out of range");
   IGB_CUDA(cudaSetDevice(device_));
   IGB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  const auto t0 = std::chrono::steady_clock::now();
-  plan_ = build_plan(*disc_, m, eta, far_order, sing_order);
-  lp_ = build_local_plan(*disc_, plan_, world, rank);
-  times_.plan_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  IGB_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
   nch_ = disc_->is_vector() ? 4 : 1;
-  const int kind = disc_->kind();
-  const int q = disc_->kind() == kMaxwell ? disc_->degree() : disc_->scalar_degree();
+  {
+    const int q = disc_->kind() == kMaxwell ? disc_->degree() : disc_->scalar_degree();
+    if (disc_->kind() == kMaxwell && (q < 1 || q > 3))
+      throw std::invalid_argument("B200 H2: Maxwell degree > 3 not instantiated");
+    if (disc_->kind() != kMaxwell && (q < 0 || q > 4))
+      throw std::invalid_argument("B200 H2: scalar space degree > 4 not instantiated");
+  }
   try {
-    if (kind == kLaplace) {
-      switch (q) {
-        case 0: assemble_impl<LapT<0>>(); break;
-        case 1: assemble_impl<LapT<1>>(); break;
-        case 2: assemble_impl<LapT<2>>(); break;
-        case 3: assemble_impl<LapT<3>>(); break;
-        case 4: assemble_impl<LapT<4>>(); break;
-        default: throw std::invalid_argument("B200 H2: scalar space degree > 4 not instantiated");
-      }
-    } else if (kind == kHelmholtz) {
-      switch (q) {
-        case 0: assemble_impl<HelmT<0>>(); break;
-        case 1: assemble_impl<HelmT<1>>(); break;
-        case 2: assemble_impl<HelmT<2>>(); break;
-        case 3: assemble_impl<HelmT<3>>(); break;
-        case 4: assemble_impl<HelmT<4>>(); break;
-        default: throw std::invalid_argument("B200 H2: scalar space degree > 4 not instantiated");
-      }
-    } else {
-      switch (q) {
-        case 1: assemble_impl<MaxT<1>>(); break;
-        case 2: assemble_impl<MaxT<2>>(); break;
-        case 3: assemble_impl<MaxT<3>>(); break;
-        default: throw std::invalid_argument("B200 H2: Maxwell degree > 3 not instantiated");
-      }
-    }
+    dispatch_kind([&](auto kt) { assemble_impl<decltype(kt)>(t_wall0); });
   } catch (...) {
-    for (void* p : allocs_) cudaFree(p);
-    allocs_.clear();
-    if (stream_) cudaStreamDestroy(stream_);
-    stream_ = nullptr;
+    cudaStreamSynchronize(aux_);
+    release_memory();
+    cudaStreamDestroy(aux_);
+    cudaStreamDestroy(stream_);
+    aux_ = stream_ = nullptr;
     throw;
   }
   times_.total_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall0).count();
@@ -1071,40 +1146,115 @@ H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, i
 H2Device::~H2Device() {
   cudaSetDevice(device_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-  for (void* p : allocs_) cudaFree(p);
-  if (h_x_pinned_) cudaFreeHost(h_x_pinned_);
-  if (h_y_pinned_) cudaFreeHost(h_y_pinned_);
+  release_memory();
+  pinned_put(h_x_pinned_);
+  pinned_put(h_y_pinned_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (side_) cudaStreamDestroy(side_);
+  if (aux_) cudaStreamDestroy(aux_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
+// Construction is a two-stage pipeline.  Stage 1 needs only the mesh: the
+// element caches / moments and the singular integrals (the bulk of the device
+// work) are launched before the block partition exists -- the singular items
+// come from the mesh topology (Discretization::singular_items).  Stage 2 builds
+// the block partition on the host while the device integrates, uploads it on a
+// second stream, and launches images, regular near blocks and the scatter of
+// the singular blocks into their near slots.
 template <class KT>
-void H2Device::assemble_impl() {
-  using S = typename KT::S;
-  constexpr int NL = KT::NL, NC = KT::NC;
+void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   const Discretization& d = *disc_;
-  const H2Plan& P = plan_;
-  if (d.local_count() != NL) throw std::logic_error("B200 H2: local count mismatch");
-  const int ne = d.element_count(), m = P.m, mm = m * m, rows = nch_ * mm;
-  const int sw = sizeof(S) / 8;
-  const cplx kap = d.kappa();
-  KParams kp;
-  kp.kr = kap.real();
-  kp.ki = kap.imag();
-  if (d.is_vector()) {
-    const cplx dw = -1.0 / (kap * kap);
-    kp.dwx = dw.real();
-    kp.dwy = dw.imag();
-  } else {
-    kp.dwx = kp.dwy = 0.0;
-  }
-  cudaEvent_t ev[10];
+  static const bool verbose = getenv("IGB_VERBOSE") != nullptr;
+  auto lap = [&](const char* what) {
+    if (verbose)
+      fprintf(stderr, "[igb ctor] %-16s %8.2f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall0).count());
+  };
+  if (d.local_count() != KT::NL) throw std::logic_error("B200 H2: local count mismatch");
+  // ---- stage 1: mesh-only data and kernels
+  std::vector<unsigned char> owned;
+  if (opt_.world > 1) owned = owned_elements(d, opt_.world, opt_.rank);
+  d.singular_items(owned.empty() ? nullptr : owned.data(), sing_items_);
+  lap("singular items");
+  auto tu = std::chrono::steady_clock::now();
+  stage_elements<KT>();
+  double up_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tu).count();
+  cudaEvent_t ev[kAsmEvents];
   for (auto& e : ev) IGB_CUDA(cudaEventCreate(&e));
+  int launched = 0;
   IGB_CUDA(cudaEventRecord(ev[0], stream_));
+  launch_element_phase<KT>(ev, launched);
+  lap("stage 1 launched");
+  // ---- stage 2: block partition on the host, overlapping the device
+  const auto t0 = std::chrono::steady_clock::now();
+  plan_ = build_plan(d, opt_.m, opt_.eta, opt_.far_order, opt_.sing_order);
+  lp_ = build_local_plan(d, plan_, opt_.world, opt_.rank);
+  times_.plan_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  lap("plan");
+  for (int c = 1; c <= 3; ++c) {  // topology items == the near list's singular pairs
+    const SingList &T = sing_items_[c], &L = lp_.sing[c];
+    if (T.ea != L.ea || T.eb != L.eb || T.map_a != L.map_a || T.map_b != L.map_b)
+      throw std::logic_error("B200 H2: singular pairs of the mesh topology differ from the near field");
+  }
+  tu = std::chrono::steady_clock::now();
+  up_stream_ = aux_;
+  alloc_ms_ = 0;
+  stage_plan<KT>();
+  up_stream_ = nullptr;
+  if (verbose) fprintf(stderr, "[igb ctor] stage-2 cudaMalloc total %.2f ms\n", alloc_ms_);
+  up_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tu).count();
+  times_.upload = up_ms;
+  IGB_CUDA(cudaEventRecord(ev[kEvUploaded], aux_));
+  IGB_CUDA(cudaStreamWaitEvent(stream_, ev[kEvUploaded], 0));
+  lap("stage 2 uploaded");
+  IGB_CUDA(cudaEventRecord(ev[kEvPlanPhase], stream_));
+  launch_plan_phase<KT>(ev, launched);
+  IGB_CUDA(cudaStreamSynchronize(stream_));
+  collect_times(ev);
+  for (auto& e : ev) cudaEventDestroy(e);
+  ++assembly_launches_count_;
+  assembly_kernels_ = launched;
+  lap("assembled");
+  alloc_ms_ = 0;
+  // ---- matvec scratch
+  const H2Plan& P = plan_;
+  const LocalPlan& Lp = lp_;
+  const int ne = d.element_count(), m = P.m, mm = m * m, rows = nch_ * mm, NL = KT::NL;
+  const int sw = sizeof(typename KT::S) / 8;
+  const size_t nn = static_cast<size_t>(P.n_nodes);
+  dx_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
+  dy_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
+  d_coef_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
+  if (Lp.world > 1) {
+    d_send_ = dalloc<double>(static_cast<size_t>(Lp.pack_max) * rows * sw);
+    d_recv_ = dalloc<double>(static_cast<size_t>(Lp.pack_max) * Lp.world * rows * sw);
+  }
+  d_up_ = dalloc<double>(nn * rows * sw);
+  d_down_ = dalloc<double>(nn * rows * sw);
+  d_loc_ = dalloc<double>(Lp.el.size() * NL * sw);
+  d_nrows_ = dalloc<double>(Lp.el.size() * NL * sw);
+  IGB_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  IGB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  IGB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaStreamSynchronize(stream_));
+  if (verbose) fprintf(stderr, "[igb ctor] scratch cudaMalloc total %.2f ms\n", alloc_ms_);
+  lap("scratch");
+}
 
-  // ---- upload
+// Stage-1 inputs: geometry cells, basis tables, DOF maps, quadrature rules and
+// the singular work lists; element-phase outputs.
+template <class KT>
+void H2Device::stage_elements() {
+  const Discretization& d = *disc_;
+  constexpr int NL = KT::NL, NC = KT::NC;
+  const int ne = d.element_count(), m = opt_.m, mm = m * m, rows = nch_ * mm;
+  const int sw = sizeof(typename KT::S) / 8;
   std::vector<double> cells(d.cells().size() * kCellStride, 0.0);
   for (size_t c = 0; c < d.cells().size(); ++c) {
     const GeomCell& gc = d.cells()[c];
@@ -1137,7 +1287,57 @@ void H2Device::assemble_impl() {
   d_tab_b_ = upload(d.is_vector() ? d.tab_q() : std::vector<double>(1, 0.0));
   d_l2g_ = upload(d.l2g());
   d_lsign_ = upload(d.lsign());
+  std::vector<double> gxf, gwf, gxs, gws;
+  gauss_rule(nfar_, gxf, gwf);
+  gauss_rule(nsing_, gxs, gws);
+  as_.gxf = upload(gxf);
+  as_.gwf = upload(gwf);
+  as_.gxs = upload(gxs);
+  as_.gws = upload(gws);
+  const std::vector<double> cheb = cheb_nodes(m);
+  as_.cheb = upload(cheb);
+  std::vector<double> lag(static_cast<size_t>(m) * nfar_);
+  {
+    std::vector<double> tmp(m);
+    for (int a = 0; a < nfar_; ++a) {
+      lagrange_all(cheb, gxf[a], tmp.data());
+      for (int i = 0; i < m; ++i) lag[i * nfar_ + a] = tmp[i];
+    }
+  }
+  as_.lag = upload(lag);
+  for (int c = 1; c <= 3; ++c) {
+    const SingList& L = sing_items_[c];
+    as_.sing[c][0] = upload(L.ea);
+    as_.sing[c][1] = upload(L.eb);
+    as_.singm[c][0] = upload(L.map_a);
+    as_.singm[c][1] = upload(L.map_b);
+    d_sing_blk_[c] = dalloc<double>(L.ea.size() * NL * NL * sw);
+  }
+  const cplx kap = d.kappa();
+  as_.kp[0] = kap.real();
+  as_.kp[1] = kap.imag();
+  if (d.is_vector()) {
+    const cplx dw = -1.0 / (kap * kap);
+    as_.kp[2] = dw.real();
+    as_.kp[3] = dw.imag();
+  }
+  const int nq = nfar_ * nfar_;
+  d_mom_ = dalloc<double>(static_cast<size_t>(ne) * NL * rows);
+  d_cpts_ = dalloc<double>(static_cast<size_t>(ne) * nq * 3);
+  d_cval_ = dalloc<double>(static_cast<size_t>(ne) * NC * nq * NL);
+  bytes_.moments = static_cast<size_t>(ne) * NL * rows * 8;
+}
+
+// Stage-2 inputs: the block partition (near / far lists, tree, transfers, DOF
+// gather) and the partition-sized outputs.
+template <class KT>
+void H2Device::stage_plan() {
+  const Discretization& d = *disc_;
+  const H2Plan& P = plan_;
   const LocalPlan& Lp = lp_;
+  constexpr int NL = KT::NL;
+  const int m = P.m, mm = m * m;
+  const int sw = sizeof(typename KT::S) / 8;
   d_near_a_ = upload(Lp.near_row);  // local row of each local near slot
   d_near_b_ = upload(Lp.near_eb);
   d_near_ea_ = upload(Lp.near_ea);
@@ -1158,7 +1358,7 @@ void H2Device::assemble_impl() {
       for (size_t i = 0; i < Lp.rank_pack_nodes[r].size(); ++i) un[static_cast<size_t>(r) * Lp.pack_max + i] = Lp.rank_pack_nodes[r][i];
     d_unpack_nodes_ = upload(un);
   }
-  d_far_a_ = upload(P.far_a);
+  if (stored_couplings()) d_far_a_ = upload(P.far_a);  // only the stored-coupling kernel reads pair rows
   d_far_b_ = upload(P.far_b);
   d_far_rs_ = upload(P.far_row_start);
   {
@@ -1182,220 +1382,164 @@ void H2Device::assemble_impl() {
   d_dof_inc_ = upload(Lp.dof_inc);
   d_tl_ = upload(P.tl);
   d_tr_ = upload(P.tr);
-  int* d_np = upload(P.node_patch);
-  int* d_nl = upload(P.node_level);
-  int* d_nsx = upload(P.node_sx);
-  int* d_nsy = upload(P.node_sy);
-  double* d_cheb = upload(P.cheb);
-  std::vector<double> gxf, gwf, gxs, gws;
-  gauss_rule(P.nfar, gxf, gwf);
-  gauss_rule(P.nsing, gxs, gws);
-  as_.gxf = upload(gxf);
-  as_.gwf = upload(gwf);
-  as_.gxs = upload(gxs);
-  as_.gws = upload(gws);
-  as_.node_patch = d_np;
-  as_.node_level = d_nl;
-  as_.node_sx = d_nsx;
-  as_.node_sy = d_nsy;
-  as_.cheb = d_cheb;
-  std::vector<double> lag(static_cast<size_t>(m) * P.nfar);
-  {
-    std::vector<double> tmp(m);
-    for (int a = 0; a < P.nfar; ++a) {
-      lagrange_all(P.cheb, gxf[a], tmp.data());
-      for (int i = 0; i < m; ++i) lag[i * P.nfar + a] = tmp[i];
-    }
-  }
-  as_.lag = upload(lag);
+  as_.node_patch = upload(P.node_patch);
+  as_.node_level = upload(P.node_level);
+  as_.node_sx = upload(P.node_sx);
+  as_.node_sy = upload(P.node_sy);
   for (int c = 1; c <= 3; ++c) {
-    const auto& L = Lp.sing[c];
-    as_.sing[c][0] = upload(L.ea);
-    as_.sing[c][1] = upload(L.eb);
-    as_.sing[c][2] = upload(L.slot_ab);
-    as_.sing[c][3] = upload(L.slot_ba);
-    as_.singm[c][0] = upload(L.map_a);
-    as_.singm[c][1] = upload(L.map_b);
+    as_.sing[c][2] = upload(Lp.sing[c].slot_ab);
+    as_.sing[c][3] = upload(Lp.sing[c].slot_ba);
   }
   as_.reg = upload(Lp.reg_slot);
-  as_.kp[0] = kp.kr;
-  as_.kp[1] = kp.ki;
-  as_.kp[2] = kp.dwx;
-  as_.kp[3] = kp.dwy;
-
   const long long nnear = static_cast<long long>(Lp.near_row.size());
   const long long nfarp = static_cast<long long>(P.far_a.size());
-  const int nf = P.nfar, nq = nf * nf;
   d_near_ = dalloc<double>(static_cast<size_t>(nnear) * NL * NL * sw);
   if (stored_couplings()) d_far_ = dalloc<double>(static_cast<size_t>(nfarp) * mm * mm * sw);
-  d_mom_ = dalloc<double>(static_cast<size_t>(ne) * NL * rows);
   d_img_ = dalloc<double>(static_cast<size_t>(P.n_nodes) * mm * 3);
-  d_cpts_ = dalloc<double>(static_cast<size_t>(ne) * nq * 3);
-  d_cval_ = dalloc<double>(static_cast<size_t>(ne) * NC * nq * NL);
   bytes_.near = static_cast<size_t>(nnear) * NL * NL * 8 * sw;
   bytes_.far = stored_couplings() ? static_cast<size_t>(nfarp) * mm * mm * 8 * sw : 0;
-  bytes_.moments = static_cast<size_t>(ne) * NL * rows * 8;
-  IGB_CUDA(cudaEventRecord(ev[1], stream_));
-  IGB_CUDA(cudaStreamSynchronize(stream_));
-  float up_ms = 0;
-  IGB_CUDA(cudaEventElapsedTime(&up_ms, ev[0], ev[1]));
-  times_.upload = up_ms;
-  run_assembly<KT>();
-  // ---- matvec scratch
-  const size_t nn = static_cast<size_t>(P.n_nodes);
-  dx_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
-  dy_ = dalloc<double>(static_cast<size_t>(d.dof_count()) * sw);
-  d_coef_ = dalloc<double>(static_cast<size_t>(ne) * NL * sw);
-  if (Lp.world > 1) {
-    d_send_ = dalloc<double>(static_cast<size_t>(Lp.pack_max) * rows * sw);
-    d_recv_ = dalloc<double>(static_cast<size_t>(Lp.pack_max) * Lp.world * rows * sw);
-  }
-  d_up_ = dalloc<double>(nn * rows * sw);
-  d_down_ = dalloc<double>(nn * rows * sw);
-  d_loc_ = dalloc<double>(Lp.el.size() * NL * sw);
-  d_nrows_ = dalloc<double>(Lp.el.size() * NL * sw);
-  IGB_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
-  IGB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
-  IGB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
-  IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
-  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  IGB_CUDA(cudaStreamSynchronize(stream_));
-  for (auto& e : ev) cudaEventDestroy(e);
 }
 
-template <class KT>
-void H2Device::run_assembly() {
-  using S = typename KT::S;
-  constexpr int NL = KT::NL, NC = KT::NC;
-  const Discretization& d = *disc_;
-  const H2Plan& P = plan_;
-  const int ne = d.element_count(), m = P.m, mm = m * m;
-  const int sw = sizeof(S) / 8;
-  (void)sw;
-  KParams kp;
-  kp.kr = as_.kp[0];
-  kp.ki = as_.kp[1];
-  kp.dwx = as_.kp[2];
-  kp.dwy = as_.kp[3];
-  const long long nfarp = static_cast<long long>(P.far_a.size());
-  const int nf = P.nfar, nq = nf * nf;
-  double* d_gxf = as_.gxf;
-  double* d_gwf = as_.gwf;
-  double* d_gxs = as_.gxs;
-  double* d_gws = as_.gws;
-  double* d_lag = as_.lag;
-  int* d_reg = as_.reg;
-  int* d_np = as_.node_patch;
-  int* d_nl = as_.node_level;
-  int* d_nsx = as_.node_sx;
-  int* d_nsy = as_.node_sy;
-  double* d_cheb = as_.cheb;
-  auto& d_sing = as_.sing;
-  auto& d_singm = as_.singm;
-  cudaEvent_t ev[10];
-  for (auto& e : ev) IGB_CUDA(cudaEventCreate(&e));
-  int launched = 0;
-  IGB_CUDA(cudaEventRecord(ev[1], stream_));
+static GeoArgs geo_args(const Discretization& d, const double* cells, const int* el_cell, const double* tab_a,
+                        const double* tab_b, const double* kp4) {
   GeoArgs g;
-  g.cells = d_cells_;
-  g.el_cell = d_el_cell_;
-  g.tab_a = d_tab_a_;
-  g.tab_b = d_tab_b_;
+  g.cells = cells;
+  g.el_cell = el_cell;
+  g.tab_a = tab_a;
+  g.tab_b = tab_b;
   g.level = d.level();
   g.epp = d.elements_per_patch();
   g.h = 1.0 / (1 << d.level());
-  g.kp = kp;
+  g.kp.kr = kp4[0];
+  g.kp.ki = kp4[1];
+  g.kp.dwx = kp4[2];
+  g.kp.dwy = kp4[3];
+  return g;
+}
 
-  // ---- K1 element caches + moments
+// K1 element caches + moments, K5 singular integrals (compact blocks)
+template <class KT>
+void H2Device::launch_element_phase(cudaEvent_t* ev, int& launched) {
+  constexpr int NL = KT::NL, NC = KT::NC;
+  const Discretization& d = *disc_;
+  const int ne = d.element_count(), m = opt_.m, nf = nfar_, nq = nf * nf;
+  const GeoArgs g = geo_args(d, d_cells_, d_el_cell_, d_tab_a_, d_tab_b_, as_.kp);
   {
     const size_t smem = (104 + KT::TABN + static_cast<size_t>(nq) * NC * NL) * 8;
     IGB_CUDA(cudaFuncSetAttribute(k_element<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     if (ne > 0) {
-      k_element<KT><<<ne, 128, smem, stream_>>>(g, nf, d_gxf, d_gwf, m, d_lag, d_cpts_, d_cval_, d_mom_);
+      k_element<KT><<<ne, 128, smem, stream_>>>(g, nf, as_.gxf, as_.gwf, m, as_.lag, d_cpts_, d_cval_, d_mom_);
       ++launched;
     }
     IGB_CUDA(cudaGetLastError());
   }
-  IGB_CUDA(cudaEventRecord(ev[2], stream_));
-  // ---- K2 images
+  IGB_CUDA(cudaEventRecord(ev[kEvElements], stream_));
+  using LY = SingLayout<KT>;
+  auto launch = [&](auto cls_tag, int evi) {
+    constexpr int CLS = decltype(cls_tag)::value;
+    const SingList& L = sing_items_[CLS];
+    if (!L.ea.empty()) {
+      SingArgs A;
+      A.n_pairs = static_cast<int>(L.ea.size());
+      A.n = nsing_;
+      A.ea = as_.sing[CLS][0];
+      A.eb = as_.sing[CLS][1];
+      A.map_a = as_.singm[CLS][0];
+      A.map_b = as_.singm[CLS][1];
+      A.gx = as_.gxs;
+      A.gw = as_.gws;
+      A.out = d_sing_blk_[CLS];
+      IGB_CUDA(cudaFuncSetAttribute(k_singular<KT, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(LY::BYTES)));
+      k_singular<KT, CLS><<<A.n_pairs, 128, LY::BYTES, stream_>>>(g, A);
+      ++launched;
+      IGB_CUDA(cudaGetLastError());
+    }
+    IGB_CUDA(cudaEventRecord(ev[evi], stream_));
+  };
+  launch(std::integral_constant<int, 3>{}, kEvCoincident);
+  launch(std::integral_constant<int, 2>{}, kEvEdge);
+  launch(std::integral_constant<int, 1>{}, kEvVertex);
+}
+
+// K2 images, K3 couplings (stored mode), K4 regular near, singular scatter
+template <class KT>
+void H2Device::launch_plan_phase(cudaEvent_t* ev, int& launched) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL, NC = KT::NC;
+  const Discretization& d = *disc_;
+  const H2Plan& P = plan_;
+  const int m = P.m, mm = m * m, nq = P.nfar * P.nfar;
+  const int sw = sizeof(S) / 8;
+  const long long nfarp = static_cast<long long>(P.far_a.size());
+  const GeoArgs g = geo_args(d, d_cells_, d_el_cell_, d_tab_a_, d_tab_b_, as_.kp);
   {
     const long long tot = static_cast<long long>(P.n_nodes) * mm;
     PatchDev pd{d_patch_info_, d_knots_};
-    k_images<<<grid_for(tot, 256), 256, 0, stream_>>>(P.n_nodes, m, d_cheb, d_np, d_nl, d_nsx, d_nsy, pd, d_cells_,
-                                                       d_img_);
+    k_images<<<grid_for(tot, 256), 256, 0, stream_>>>(P.n_nodes, m, as_.cheb, as_.node_patch, as_.node_level,
+                                                       as_.node_sx, as_.node_sy, pd, d_cells_, d_img_);
     ++launched;
     IGB_CUDA(cudaGetLastError());
   }
-  IGB_CUDA(cudaEventRecord(ev[3], stream_));
-  // ---- K3 couplings (stored mode only; fused mode evaluates them in the matvec)
-  if (nfarp > 0 && stored_couplings()) {
-    k_couplings<KT><<<148 * 16, 256, 0, stream_>>>(nfarp, mm, d_far_a_, d_far_b_, d_img_, kp, d_far_);
+  IGB_CUDA(cudaEventRecord(ev[kEvImages], stream_));
+  if (nfarp > 0 && stored_couplings()) {  // fused mode evaluates the couplings inside the matvec
+    k_couplings<KT><<<148 * 16, 256, 0, stream_>>>(nfarp, mm, d_far_a_, d_far_b_, d_img_, g.kp, d_far_);
     ++launched;
     IGB_CUDA(cudaGetLastError());
   }
-  IGB_CUDA(cudaEventRecord(ev[4], stream_));
-  // ---- K4 regular near
+  IGB_CUDA(cudaEventRecord(ev[kEvCouplings], stream_));
   if (!lp_.reg_slot.empty()) {
     const size_t smem = static_cast<size_t>(NC) * nq * NL * 8 * sw;
     IGB_CUDA(cudaFuncSetAttribute(k_regular<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     if (smem > 200 * 1024) throw std::invalid_argument("B200 H2: far quadrature order too large");
     k_regular<KT><<<static_cast<unsigned>(lp_.reg_slot.size()), 128, smem, stream_>>>(
-        d_reg, d_near_a_, d_near_b_, d_near_rs_, d_near_ea_, nq, d_cpts_, d_cval_, kp, d_near_);
+        as_.reg, d_near_a_, d_near_b_, d_near_rs_, d_near_ea_, nq, d_cpts_, d_cval_, g.kp, d_near_);
     ++launched;
     IGB_CUDA(cudaGetLastError());
   }
-  IGB_CUDA(cudaEventRecord(ev[5], stream_));
-  // ---- K5 singular near, batched by class
-  {
-    using LY = SingLayout<KT>;
-    if (P.nsing > 64) throw std::invalid_argument("gauss_rule: order out of range");
-    if (P.nsing > 16) throw std::invalid_argument("B200 H2: singular order > 16 not supported (32-bit point index)");
-    auto launch = [&](auto cls_tag, int c, int evi) {
-      constexpr int CLS = decltype(cls_tag)::value;
-      const auto& L = lp_.sing[c];
-      if (!L.ea.empty()) {
-        SingArgs A;
-        A.n_pairs = static_cast<int>(L.ea.size());
-        A.n = P.nsing;
-        A.ea = d_sing[c][0];
-        A.eb = d_sing[c][1];
-        A.slot_ab = d_sing[c][2];
-        A.slot_ba = d_sing[c][3];
-        A.map_a = d_singm[c][0];
-        A.map_b = d_singm[c][1];
-        A.gx = d_gxs;
-        A.gw = d_gws;
-        A.near_a = d_near_a_;
-        A.near_rs = d_near_rs_;
-        A.near = d_near_;
-        IGB_CUDA(cudaFuncSetAttribute(k_singular<KT, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(LY::BYTES)));
-        k_singular<KT, CLS><<<A.n_pairs, 128, LY::BYTES, stream_>>>(g, A);
-        ++launched;
-        IGB_CUDA(cudaGetLastError());
-      }
-      IGB_CUDA(cudaEventRecord(ev[evi], stream_));
-    };
-    launch(std::integral_constant<int, 3>{}, 3, 6);
-    launch(std::integral_constant<int, 2>{}, 2, 7);
-    launch(std::integral_constant<int, 1>{}, 1, 8);
+  IGB_CUDA(cudaEventRecord(ev[kEvRegular], stream_));
+  for (int c = 3; c >= 1; --c) {
+    const size_t n = lp_.sing[c].ea.size();
+    if (n == 0) continue;
+    k_sing_scatter<S, NL><<<static_cast<unsigned>(n), 128, 0, stream_>>>(
+        as_.sing[c][2], as_.sing[c][3], d_near_a_, d_near_rs_, reinterpret_cast<const S*>(d_sing_blk_[c]),
+        reinterpret_cast<S*>(d_near_));
+    ++launched;
+    IGB_CUDA(cudaGetLastError());
   }
-  IGB_CUDA(cudaStreamSynchronize(stream_));
+  IGB_CUDA(cudaEventRecord(ev[kEvScatter], stream_));
+}
+
+void H2Device::collect_times(cudaEvent_t* ev) {
   float ms = 0;
   auto el = [&](int a, int b) {
     IGB_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
     return static_cast<double>(ms);
   };
-  times_.elements = el(1, 2);
-  times_.images = el(2, 3);
-  times_.couplings = el(3, 4);
-  times_.regular = el(4, 5);
-  times_.singular[3] = el(5, 6);
-  times_.singular[2] = el(6, 7);
-  times_.singular[1] = el(7, 8);
-  times_.total_device = el(1, 8);
+  times_.elements = el(kEvStart, kEvElements);
+  times_.singular[3] = el(kEvElements, kEvCoincident);
+  times_.singular[2] = el(kEvCoincident, kEvEdge);
+  times_.singular[1] = el(kEvEdge, kEvVertex);
+  times_.images = el(kEvPlanPhase, kEvImages);
+  times_.couplings = el(kEvImages, kEvCouplings);
+  times_.regular = el(kEvCouplings, kEvRegular);
+  times_.scatter = el(kEvRegular, kEvScatter);
+  // kernel time (the construction-time gap waiting for the host partition excluded)
+  times_.total_device = el(kEvStart, kEvVertex) + el(kEvPlanPhase, kEvScatter);
+}
+
+template <class KT>
+void H2Device::run_assembly() {
+  cudaEvent_t ev[kAsmEvents];
+  for (auto& e : ev) IGB_CUDA(cudaEventCreate(&e));
+  int launched = 0;
+  IGB_CUDA(cudaEventRecord(ev[kEvStart], stream_));
+  launch_element_phase<KT>(ev, launched);
+  IGB_CUDA(cudaEventRecord(ev[kEvUploaded], stream_));
+  IGB_CUDA(cudaEventRecord(ev[kEvPlanPhase], stream_));
+  launch_plan_phase<KT>(ev, launched);
+  IGB_CUDA(cudaStreamSynchronize(stream_));
+  collect_times(ev);
   for (auto& e : ev) cudaEventDestroy(e);
   ++assembly_launches_count_;
   assembly_kernels_ = launched;
@@ -1403,31 +1547,7 @@ void H2Device::run_assembly() {
 
 double H2Device::reassemble() {
   IGB_CUDA(cudaSetDevice(device_));
-  const int kind = disc_->kind();
-  const int q = kind == kMaxwell ? disc_->degree() : disc_->scalar_degree();
-  if (kind == kLaplace) {
-    switch (q) {
-      case 0: run_assembly<LapT<0>>(); break;
-      case 1: run_assembly<LapT<1>>(); break;
-      case 2: run_assembly<LapT<2>>(); break;
-      case 3: run_assembly<LapT<3>>(); break;
-      default: run_assembly<LapT<4>>(); break;
-    }
-  } else if (kind == kHelmholtz) {
-    switch (q) {
-      case 0: run_assembly<HelmT<0>>(); break;
-      case 1: run_assembly<HelmT<1>>(); break;
-      case 2: run_assembly<HelmT<2>>(); break;
-      case 3: run_assembly<HelmT<3>>(); break;
-      default: run_assembly<HelmT<4>>(); break;
-    }
-  } else {
-    switch (q) {
-      case 1: run_assembly<MaxT<1>>(); break;
-      case 2: run_assembly<MaxT<2>>(); break;
-      default: run_assembly<MaxT<3>>(); break;
-    }
-  }
+  dispatch_kind([&](auto kt) { run_assembly<decltype(kt)>(); });
   return times_.total_device;
 }
 
@@ -1755,8 +1875,8 @@ void H2Device::apply_host(const double* x, double* y) {
   const size_t bytes = static_cast<size_t>(dim()) * (is_complex() ? 16 : 8);
   IGB_CUDA(cudaSetDevice(device_));
   if (!h_x_pinned_) {
-    IGB_CUDA(cudaMallocHost(&h_x_pinned_, bytes));
-    IGB_CUDA(cudaMallocHost(&h_y_pinned_, bytes));
+    h_x_pinned_ = static_cast<double*>(pinned_get(bytes));
+    h_y_pinned_ = static_cast<double*>(pinned_get(bytes));
   }
   std::memcpy(h_x_pinned_, x, bytes);
   IGB_CUDA(cudaMemcpyAsync(dx_, h_x_pinned_, bytes, cudaMemcpyHostToDevice, stream_));
@@ -1799,21 +1919,32 @@ void H2Device::couplings(long long first, long long count, double* out) const {
     return;
   }
   // fused mode: evaluate the requested couplings with the assembly kernel
+  // (the pair rows are not resident in this mode: upload the slice)
   double* tmp = nullptr;
+  int* rows = nullptr;
   IGB_CUDA(cudaMalloc(&tmp, count * per * 8));
+  if (cudaMalloc(&rows, count * sizeof(int)) != cudaSuccess) {
+    cudaFree(tmp);
+    throw std::runtime_error("couplings: out of device memory");
+  }
+  const cudaError_t e0 = cudaMemcpy(rows, plan_.far_a.data() + first, count * sizeof(int), cudaMemcpyHostToDevice);
   KParams kp;
   kp.kr = as_.kp[0];
   kp.ki = as_.kp[1];
   kp.dwx = as_.kp[2];
   kp.dwy = as_.kp[3];
   const int mm = plan_.m * plan_.m;
-  if (is_complex())
-    k_couplings<HelmT<0>><<<148 * 16, 256, 0, stream_>>>(count, mm, d_far_a_ + first, d_far_b_ + first, d_img_, kp, tmp);
-  else
-    k_couplings<LapT<0>><<<148 * 16, 256, 0, stream_>>>(count, mm, d_far_a_ + first, d_far_b_ + first, d_img_, kp, tmp);
+  if (e0 == cudaSuccess) {
+    if (is_complex())
+      k_couplings<HelmT<0>><<<148 * 16, 256, 0, stream_>>>(count, mm, rows, d_far_b_ + first, d_img_, kp, tmp);
+    else
+      k_couplings<LapT<0>><<<148 * 16, 256, 0, stream_>>>(count, mm, rows, d_far_b_ + first, d_img_, kp, tmp);
+  }
   const cudaError_t e1 = cudaStreamSynchronize(stream_);
   const cudaError_t e2 = cudaMemcpy(out, tmp, count * per * 8, cudaMemcpyDeviceToHost);
   cudaFree(tmp);
+  cudaFree(rows);
+  IGB_CUDA(e0);
   IGB_CUDA(e1);
   IGB_CUDA(e2);
 }

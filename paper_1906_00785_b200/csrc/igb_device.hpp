@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <memory>
 #include <vector>
 
@@ -12,7 +13,7 @@ namespace igb {
 
 struct AssemblyTimes {  // milliseconds, CUDA events on the assembly stream
   double plan_host = 0, upload = 0, elements = 0, images = 0, couplings = 0, regular = 0,
-         singular[4] = {0, 0, 0, 0}, total_device = 0, total_wall = 0;
+         singular[4] = {0, 0, 0, 0}, total_device = 0, total_wall = 0, scatter = 0;
 };
 
 struct DeviceBytes {
@@ -77,8 +78,16 @@ class H2Device {
   void images(double* out) const;                                         // [node][nu][3]
 
  private:
-  template <class KT> void assemble_impl();
+  template <class KT> void assemble_impl(std::chrono::steady_clock::time_point t_wall0);
+  template <class KT> void stage_elements();
+  template <class KT> void stage_plan();
+  template <class KT> void launch_element_phase(cudaEvent_t* ev, int& launched);
+  template <class KT> void launch_plan_phase(cudaEvent_t* ev, int& launched);
   template <class KT> void run_assembly();
+  void collect_times(cudaEvent_t* ev);
+  // assembly events
+  enum { kEvStart, kEvElements, kEvCoincident, kEvEdge, kEvVertex, kEvUploaded, kEvPlanPhase, kEvImages,
+         kEvCouplings, kEvRegular, kEvScatter, kAsmEvents };
   template <class KT> void enqueue_apply(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev);
   template <class KT> void enqueue_phase1(const double* x, double* send, cudaStream_t s, cudaEvent_t* pev, int& n);
   template <class KT> void enqueue_phase2(const double* recv, double* y, cudaStream_t s, cudaEvent_t* pev, int& n);
@@ -89,13 +98,24 @@ class H2Device {
   H2Plan plan_;
   LocalPlan lp_;
   int device_ = 0, nch_ = 1, flags_ = 0;
+  struct Opts {
+    int m;
+    double eta;
+    int far_order, sing_order, world, rank;
+  } opt_{};
+  int nfar_ = 0, nsing_ = 0;
+  SingList sing_items_[4];          // singular items from the mesh topology (stage 1)
+  double* d_sing_blk_[4] = {};      // their blocks [item][la][lb], Scalar
   cudaStream_t stream_ = nullptr;
+  cudaStream_t aux_ = nullptr;      // stage-2 uploads (overlap the stage-1 kernels)
+  cudaStream_t up_stream_ = nullptr;
   AssemblyTimes times_;
   DeviceBytes bytes_;
 
   // device arrays (raw allocations, owned)
   std::vector<void*> allocs_;
-  template <class T> T* dalloc(size_t n);
+  template <class T> T* dalloc(size_t n);  // stream-ordered, from the per-device pool
+  void release_memory();
   template <class T> T* upload(const std::vector<T>& v);
 
   // geometry / space
@@ -139,6 +159,7 @@ class H2Device {
   int apply_launches_ = 0, phase1_launches_ = 0;
   int assembly_kernels_ = 0, assembly_launches_count_ = 0;
   size_t upload_bytes_ = 0;
+  double alloc_ms_ = 0;
   struct AsmState {
     double *gxf = nullptr, *gwf = nullptr, *gxs = nullptr, *gws = nullptr, *lag = nullptr, *cheb = nullptr;
     int *reg = nullptr, *node_patch = nullptr, *node_level = nullptr, *node_sx = nullptr, *node_sy = nullptr;

@@ -926,6 +926,85 @@ PairInfo Discretization::classify_pair(int ea, int eb) const {
   return info;
 }
 
+void Discretization::singular_items(const unsigned char* owned, SingList out[4]) const {
+  const int ne = element_count(), n = 1 << level_, np = geometry().patch_count();
+  // patches sharing an edge / a corner with each patch
+  std::vector<std::vector<int>> edge_nb(np), corner_nb(np);
+  for (int p = 0; p < np; ++p)
+    for (int q = 0; q < np; ++q) {
+      if (!cross_edges_[p][q].empty()) edge_nb[p].push_back(q);
+      if (!cross_corners_[p][q].empty()) corner_nb[p].push_back(q);
+    }
+  auto edge_element = [&](int patch, int edge, int s) {  // element at position s along a patch edge
+    switch (edge) {
+      case 0: return element_index(patch, s, 0);
+      case 1: return element_index(patch, n - 1, s);
+      case 2: return element_index(patch, s, n - 1);
+      default: return element_index(patch, 0, s);
+    }
+  };
+  auto corner_element = [&](int patch, int corner) {
+    return element_index(patch, (corner == 1 || corner == 3) ? n - 1 : 0, corner >= 2 ? n - 1 : 0);
+  };
+  int nt = 1;
+#ifdef _OPENMP
+  nt = omp_get_max_threads();
+#endif
+  std::vector<SingList> part(static_cast<size_t>(nt) * 4);
+#pragma omp parallel num_threads(nt)
+  {
+    int t = 0;
+#ifdef _OPENMP
+    t = omp_get_thread_num();
+#endif
+    const int e0 = static_cast<int>(static_cast<long long>(ne) * t / nt);
+    const int e1 = static_cast<int>(static_cast<long long>(ne) * (t + 1) / nt);
+    std::vector<int> cand;
+    for (int ea = e0; ea < e1; ++ea) {
+      const Element& a = elements_[ea];
+      cand.clear();
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int x = a.ix + dx, y = a.iy + dy;
+          if (x >= 0 && x < n && y >= 0 && y < n) cand.push_back(element_index(a.patch, x, y));
+        }
+      for (int pb : edge_nb[a.patch])
+        for (const auto& ce : cross_edges_[a.patch][pb]) {
+          if (!element_on_edge(ce.edge_a, a.ix, a.iy, n)) continue;
+          const int sa = grid_pos_on_edge(ce.edge_a, a.ix, a.iy);
+          for (int sb = std::max(0, sa - 1); sb <= std::min(n - 1, sa + 1); ++sb)
+            cand.push_back(edge_element(pb, ce.edge_b, ce.reversed ? n - 1 - sb : sb));
+        }
+      for (int pb : corner_nb[a.patch])
+        for (const auto& cc : cross_corners_[a.patch][pb])
+          if (element_at_corner(cc.corner_a, a.ix, a.iy, n)) cand.push_back(corner_element(pb, cc.corner_b));
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      for (int eb : cand) {
+        if (eb < ea || (owned && !owned[ea] && !owned[eb])) continue;
+        const PairInfo info = classify_pair(ea, eb);
+        if (info.cls == kFar) continue;
+        SingList& L = part[static_cast<size_t>(t) * 4 + info.cls];
+        L.ea.push_back(ea);
+        L.eb.push_back(eb);
+        L.map_a.push_back(static_cast<uint8_t>(info.map_a.bits()));
+        L.map_b.push_back(static_cast<uint8_t>(info.map_b.bits()));
+      }
+    }
+  }
+  for (int c = 1; c <= 3; ++c) {
+    SingList& L = out[c];
+    L = SingList{};
+    for (int t = 0; t < nt; ++t) {
+      const SingList& S = part[static_cast<size_t>(t) * 4 + c];
+      L.ea.insert(L.ea.end(), S.ea.begin(), S.ea.end());
+      L.eb.insert(L.eb.end(), S.eb.begin(), S.eb.end());
+      L.map_a.insert(L.map_a.end(), S.map_a.begin(), S.map_a.end());
+      L.map_b.insert(L.map_b.end(), S.map_b.begin(), S.map_b.end());
+    }
+  }
+}
+
 // ---------------------------------------------------------- quadrature
 void gauss_rule(int n, std::vector<double>& nodes, std::vector<double>& weights) {  // quadrature.cpp:15-50
   if (n < 1 || n > 64) throw std::invalid_argument("gauss_rule: order out of range");
@@ -974,6 +1053,15 @@ void lagrange_all(const std::vector<double>& nodes, double x, double* out) {  //
 }
 
 // ------------------------------------------------------------ H2 plan
+void check_h2_options(const Discretization& d, int m, double eta, int far_order, int sing_order, int* nfar,
+                      int* nsing) {
+  if (m < 2) throw std::invalid_argument("H2Matrix: interpolation degree m < 2");
+  if (!(eta > 0)) throw std::invalid_argument("H2Matrix: eta must be positive");
+  *nfar = far_order > 0 ? far_order : d.degree() + 2;
+  *nsing = sing_order > 0 ? sing_order : d.degree() + 3;
+  if (*nfar > 64 || *nsing > 64) throw std::invalid_argument("gauss_rule: order out of range");
+}
+
 H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order) {
   static const bool verbose = getenv("IGB_VERBOSE") != nullptr;
   auto tp = std::chrono::steady_clock::now();
@@ -983,14 +1071,10 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
     fprintf(stderr, "[igb plan] %-14s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - tp).count());
     tp = now;
   };
-  if (m < 2) throw std::invalid_argument("H2Matrix: interpolation degree m < 2");
-  if (!(eta > 0)) throw std::invalid_argument("H2Matrix: eta must be positive");
   H2Plan P;
+  check_h2_options(d, m, eta, far_order, sing_order, &P.nfar, &P.nsing);
   P.m = m;
   P.eta = eta;
-  P.nfar = far_order > 0 ? far_order : d.degree() + 2;
-  P.nsing = sing_order > 0 ? sing_order : d.degree() + 3;
-  if (P.nfar > 64 || P.nsing > 64) throw std::invalid_argument("gauss_rule: order out of range");
   const int L = d.level(), np = d.geometry().patch_count(), ne = d.element_count();
   P.depth = L;
   P.n_patches = np;
@@ -1259,22 +1343,31 @@ int node_cluster(const H2Plan& P, int node) {
   return 4 * P.node_patch[node] + sx + 2 * sy;
 }
 
+std::vector<unsigned char> owned_elements(const Discretization& d, int world, int rank) {
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("partition: bad rank/world");
+  const int ncl = d.level() >= 1 ? 4 * d.geometry().patch_count() : 1;
+  const int c0 = static_cast<int>(static_cast<long long>(ncl) * rank / world);
+  const int c1 = static_cast<int>(static_cast<long long>(ncl) * (rank + 1) / world);
+  const int ne = d.element_count(), n = 1 << d.level();
+  std::vector<unsigned char> own(ne, 0);
+  for (int e = 0; e < ne; ++e) {
+    const Element& el = d.element(e);
+    const int cl = d.level() >= 1 ? 4 * el.patch + (el.ix >= n / 2 ? 1 : 0) + 2 * (el.iy >= n / 2 ? 1 : 0) : 0;
+    own[e] = cl >= c0 && cl < c1;
+  }
+  return own;
+}
+
 RowPartition partition_rows(const Discretization& d, const H2Plan& P, int world, int rank) {
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("partition: bad rank/world");
   RowPartition r;
   const int ncl = d.level() >= 1 ? 4 * P.n_patches : 1;
   r.c0 = static_cast<int>(static_cast<long long>(ncl) * rank / world);
   r.c1 = static_cast<int>(static_cast<long long>(ncl) * (rank + 1) / world);
-  const int ne = d.element_count(), n = 1 << d.level();
-  r.owns_element.assign(ne, 0);
-  for (int e = 0; e < ne; ++e) {
-    const Element& el = d.element(e);
-    const int cl = d.level() >= 1 ? 4 * el.patch + (el.ix >= n / 2 ? 1 : 0) + 2 * (el.iy >= n / 2 ? 1 : 0) : 0;
-    if (cl >= r.c0 && cl < r.c1) {
-      r.owns_element[e] = 1;
-      r.elements.push_back(e);
-    }
-  }
+  const int ne = d.element_count();
+  r.owns_element = owned_elements(d, world, rank);
+  for (int e = 0; e < ne; ++e)
+    if (r.owns_element[e]) r.elements.push_back(e);
   for (int e : r.elements) r.near_count += P.near_row_start[e + 1] - P.near_row_start[e];
   for (size_t q = 0; q < P.far_a.size(); ++q) {
     const int cl = node_cluster(P, P.far_a[q]);

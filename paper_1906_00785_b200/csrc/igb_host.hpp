@@ -122,6 +122,14 @@ struct GeomCell {
   double coef[4][kMaxGeomDeg + 1][kMaxGeomDeg + 1];
 };
 
+// Unique singular work items of one class (ea <= eb): element ids, map bits
+// and, once a block partition exists, the two near-list output slots (slot of
+// (ea,eb) and of (eb,ea); equal for coincident pairs).
+struct SingList {
+  std::vector<int> ea, eb, slot_ab, slot_ba;
+  std::vector<uint8_t> map_a, map_b;
+};
+
 // Discrete space (spaces.hpp:37-105).
 class Discretization {
  public:
@@ -144,6 +152,12 @@ class Discretization {
   const std::vector<int>& l2g() const { return l2g_; }
   const std::vector<double>& lsign() const { return lsign_; }
   PairInfo classify_pair(int ea, int eb) const;  // spaces.cpp:309-394
+  // The singular items (classify_pair class >= 1, ea <= eb) enumerated from the
+  // mesh topology alone -- no block tree: same-patch neighbours, elements along
+  // shared patch edges and at shared patch corners.  Ascending (ea, eb): the
+  // order build_plan extracts them from the sorted near list.  owned != null:
+  // only items with ea or eb owned (a rank's block rows).  No slots.
+  void singular_items(const unsigned char* owned, SingList out[4]) const;
 
   // GPU tables ---------------------------------------------------------
   // geometry cells and per-element cell index
@@ -218,10 +232,8 @@ struct H2Plan {
   // unique singular work items per class (ea <= eb): element ids, map bits,
   // and the two output slots (slot of (ea,eb) and of (eb,ea); equal for
   // coincident pairs)
-  struct SingList {
-    std::vector<int> ea, eb, slot_ab, slot_ba;
-    std::vector<uint8_t> map_a, map_b;
-  } sing[4];
+  using SingList = igb::SingList;
+  SingList sing[4];
   std::vector<int> reg_slot;  // regular near pairs (slot into near list)
   // DOF gather incidence for the deterministic scatter: for dof d the
   // (e*nl + l) entries in ascending order, sign folded in by the device
@@ -234,6 +246,10 @@ struct H2Plan {
   }
 };
 H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order);
+// Option checks of build_plan (h2.hpp:60 ctor) and the quadrature orders it
+// derives (far: degree + 2, singular: degree + 3 unless given).
+void check_h2_options(const Discretization& d, int m, double eta, int far_order, int sing_order, int* nfar,
+                      int* nsing);
 
 // Row-cluster partition: rank owns level-1 clusters [c0, c1)
 // (cluster = 4 * patch + sx + 2 * sy); with level 0 the whole operator sits
@@ -246,6 +262,8 @@ struct RowPartition {
   long long near_count = 0, far_count = 0;
 };
 int node_cluster(const H2Plan& P, int node);  // level-1 cluster of a node, -1 for roots
+// element ownership of the row partition (no block tree needed)
+std::vector<unsigned char> owned_elements(const Discretization& d, int world, int rank);
 RowPartition partition_rows(const Discretization& d, const H2Plan& P, int world, int rank);
 
 // Rank-local view of the plan (identity for world == 1): owned block rows,

@@ -59,7 +59,7 @@ class _Storage(ctypes.Structure):
 class _Times(ctypes.Structure):
     _fields_ = [(n, ctypes.c_double) for n in ("plan_host_ms", "upload_ms", "elements_ms", "images_ms",
                                                "couplings_ms", "regular_ms", "coincident_ms", "edge_ms",
-                                               "vertex_ms", "device_total_ms", "wall_total_ms")]
+                                               "vertex_ms", "device_total_ms", "wall_total_ms", "scatter_ms")]
 
 
 class _SolverOpts(ctypes.Structure):
@@ -89,7 +89,8 @@ SYMBOLS = (
     "igb_h2_gmres", "igb_h2_cg", "igb_rhs_points", "igb_rhs_assemble", "igb_potential",
     "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_counts", "igb_plan_near_pairs",
-    "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
+    "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
+    "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
 )
 
 
@@ -156,6 +157,7 @@ def lib():
     L.igb_plan_class_counts.argtypes = [vp, P(i64)]
     L.igb_plan_partition.argtypes = [vp, i32, i32, P(i32), P(i32), P(i32), P(i64), P(i64)]
     L.igb_plan_owned.argtypes = [vp, i32, i32, P(ctypes.c_ubyte), P(ctypes.c_ubyte)]
+    L.igb_plan_singular_items.argtypes = [vp, i32, i32, P(ctypes.c_longlong), P(i32)]
     L.igb_plan_destroy.argtypes = [vp]
     L.igb_plan_destroy.restype = None
     L.igb_h2_gmres.argtypes = [vp, P(f64), P(f64), P(_SolverOpts), P(_SolveStats)]
@@ -408,6 +410,16 @@ class H2Plan:
         nm = np.zeros(self.node_count, dtype=np.uint8)
         _check(lib().igb_plan_owned(self._h, int(world), int(rank), _p(em, ctypes.c_ubyte), _p(nm, ctypes.c_ubyte)))
         return em.astype(bool), nm.astype(bool)
+
+    def singular_items(self, world=1, rank=0):
+        """(counts [regular, vertex, edge, coincident], equal): the singular items
+        of one rank enumerated from the mesh topology alone, and whether they
+        equal the near list's singular pairs (the device integrates the former
+        before the block partition exists)."""
+        counts = (ctypes.c_longlong * 4)()
+        bad = ctypes.c_int()
+        _check(lib().igb_plan_singular_items(self._h, int(world), int(rank), counts, ctypes.byref(bad)))
+        return list(counts), bad.value == 0
 
 
 class H2Matrix:

@@ -89,6 +89,29 @@ def test_class_counts_c2_structure(igb):
     assert cc == dict(regular=339072, vertex=98280 // 2, edge=98304 // 2, coincident=24576)
 
 
+@pytest.mark.parametrize("geom,kind,P,L", [("sphere", "laplace", 3, 0), ("sphere", "laplace", 1, 1),
+                                           ("sphere", "laplace", 3, 4), ("sphere", "maxwell", 2, 3),
+                                           ("square", "laplace", 2, 3), ("square", "helmholtz", 1, 0)])
+def test_singular_items_from_topology(igb, geom, kind, P, L):
+    """The device integrates the singular pairs before the block partition
+    exists, enumerating them from the mesh topology; they must be exactly the
+    near list's singular pairs (same order, same maps) on every rank."""
+    g = igb.make_sphere() if geom == "sphere" else igb.make_square()
+    d = igb.Discretization(g, _pde(igb, kind), P, 1, L)
+    plan = igb.H2Plan(d, igb.H2Options(m=4))
+    cc = plan.class_counts()
+    counts, equal = plan.singular_items()
+    assert equal
+    assert counts == [cc["regular"], cc["vertex"], cc["edge"], cc["coincident"]]
+    for world in (2, 3, 5):
+        tot = np.zeros(4, dtype=np.int64)
+        for r in range(world):
+            c, equal = plan.singular_items(world, r)
+            assert equal, (world, r)
+            tot += c
+        assert tot[3] == cc["coincident"]  # coincident items belong to exactly one rank
+
+
 def test_row_partition_covers_everything(igb):
     d = igb.Discretization(igb.make_sphere(), igb.Pde.laplace(), 2, 1, 3)
     plan = igb.H2Plan(d, igb.H2Options(m=8))
