@@ -220,20 +220,83 @@ __global__ void __launch_bounds__(128) k_regular(const int* __restrict__ slots, 
 
 // ---------------------------------------------------- K5: singular near
 // Regularised relative-coordinate rules generated in-register
-// (quadrature.cpp:82-177); one CTA per unique pair (ea <= eb), the block and
-// its transpose written to both ordered slots (pair_integration.hpp:139-148).
+// (quadrature.cpp:82-177) line by line (rule_line); one CTA per unique pair
+// (ea <= eb) writing the compact block, which k_sing_scatter places in the
+// two ordered slots (pair_integration.hpp:139-148).
+
+// Sum-factorised geometry jet.  Setup (once per rule line, element, homogeneous
+// component): with the fixed cell coordinate f, A_o = sum_k c[o][k] f^k and
+// B_o its derivative in f (the inner Horner loops of jet<4>); for a moving v
+// the coefficients are read as c[j][i] (o = j), for a moving u as c[i][j].
+__device__ __forceinline__ void jet_setup(const double* __restrict__ comp, int v_moves, double f,
+                                          double* __restrict__ out) {
+  const int so = v_moves ? 5 : 1, sk = v_moves ? 1 : 5;
+#pragma unroll
+  for (int o = 0; o <= kMaxGeomDeg; ++o) {
+    double r = comp[o * so + kMaxGeomDeg * sk], rp = 0.0;
+#pragma unroll
+    for (int k = kMaxGeomDeg - 1; k >= 0; --k) {
+      rp = fma(rp, f, r);
+      r = fma(r, f, comp[o * so + k * sk]);
+    }
+    out[o] = r;
+    out[5 + o] = rp;
+  }
+}
+// Point of a line from its setup at the moving coordinate y: the outer Horner
+// loop of jet<4> (the same arithmetic when v moves) and the rational quotient.
+__device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_moves, double y, double x[3],
+                                         double du[3], double dv[3]) {
+  double N[4], Ns[4], Nt[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* A = st + c * 10;
+    double n = 0.0, ny = 0.0, nx = 0.0;
+#pragma unroll
+    for (int o = kMaxGeomDeg; o >= 0; --o) {
+      ny = fma(ny, y, n);
+      n = fma(n, y, A[o]);
+      nx = fma(nx, y, A[5 + o]);
+    }
+    N[c] = n;
+    Ns[c] = v_moves ? nx : ny;
+    Nt[c] = v_moves ? ny : nx;
+  }
+  const double iw = 1.0 / N[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    x[k] = N[k] * iw;
+    du[k] = (Ns[k] - x[k] * Ns[3]) * iw;
+    dv[k] = (Nt[k] - x[k] * Nt[3]) * iw;
+  }
+}
+
+// Exact small-integer division by the (runtime) rule order n: float
+// reciprocal estimate, then one correction step either way (x < 2^24).
+__device__ __forceinline__ int div_n(int x, int n, float rn) {
+  int q = __float2int_rz(__int2float_rn(x) * rn);
+  q += (q + 1) * n <= x;
+  q -= q * n > x;
+  return q;
+}
+
+// One rule line (fixed sector, i1, i2, i3; i4 runs): after the element maps,
+// every coordinate is affine in gx[i4] -- (ua, va, ub, vb) = c0 + c1 gx[i4] --
+// and the weight is wl * gw[i4] (the rules of quadrature.cpp:82-177 with the
+// maps of quadrature.hpp:25-29 folded in).
 template <int CLS>
-__device__ __forceinline__ void rule_point(int p, int n, const double* gx, const double* gw, double& ua,
-                                           double& va, double& ub, double& vb, double& w) {
-  const int i4 = p % n;
-  p /= n;
-  const int i3 = p % n;
-  p /= n;
-  const int i2 = p % n;
-  p /= n;
-  const int i1 = p % n;
-  const int sec = p / n;
-  const double wp = gw[i1] * gw[i2] * gw[i3] * gw[i4];
+__device__ __forceinline__ void rule_line(int line, int n, float rn, const double* gx, const double* gw, int ma,
+                                          int mb, double c0[4], double c1[4], double& wl) {
+  int q = div_n(line, n, rn);
+  const int i3 = line - q * n;
+  int r = q;
+  q = div_n(r, n, rn);
+  const int i2 = r - q * n;
+  r = q;
+  q = div_n(r, n, rn);
+  const int i1 = r - q * n;
+  const int sec = q;
+  const double w3 = gw[i1] * gw[i2] * gw[i3];
   if constexpr (CLS == 3) {  // coincident (quadrature.cpp:82-111)
     const int axis = sec >> 2;
     const double dir = (sec & 2) ? -1.0 : 1.0, sgn = (sec & 1) ? -1.0 : 1.0;
@@ -248,17 +311,17 @@ __device__ __forceinline__ void rule_point(int p, int n, const double* gx, const
     }
     const double lx = 1.0 - fabs(z1), ly = 1.0 - fabs(z2);
     const double x1 = fmax(0.0, -z1) + lx * gx[i3];
-    const double x2 = fmax(0.0, -z2) + ly * gx[i4];
-    ua = x1;
-    va = x2;
-    ub = x1 + z1;
-    vb = x2 + z2;
-    w = wp * t * lx * ly;
+    const double x2 = fmax(0.0, -z2);
+    c0[0] = x1;      c1[0] = 0.0;
+    c0[1] = x2;      c1[1] = ly;
+    c0[2] = x1 + z1; c1[2] = 0.0;
+    c0[3] = x2 + z2; c1[3] = ly;
+    wl = w3 * t * lx * ly;
   } else if constexpr (CLS == 2) {  // edge (quadrature.cpp:113-149)
     const int kind = sec >> 1;
     const double sgn = (sec & 1) ? -1.0 : 1.0;
     const double t = gx[i1], a = gx[i2], b = gx[i3];
-    double d, jac;
+    double d, jac, va, vb;
     if (kind == 0) {
       va = t; vb = t * b; d = sgn * t * a; jac = t * t * (1.0 - t * a);
     } else if (kind == 1) {
@@ -266,29 +329,35 @@ __device__ __forceinline__ void rule_point(int p, int n, const double* gx, const
     } else {
       d = sgn * t; va = t * a; vb = t * b; jac = t * t * (1.0 - t);
     }
-    ua = fmax(0.0, -d) + (1.0 - fabs(d)) * gx[i4];
-    ub = ua + d;
-    w = wp * jac;
+    const double u0 = fmax(0.0, -d), ul = 1.0 - fabs(d);
+    c0[0] = u0;     c1[0] = ul;
+    c0[1] = va;     c1[1] = 0.0;
+    c0[2] = u0 + d; c1[2] = ul;
+    c0[3] = vb;     c1[3] = 0.0;
+    wl = w3 * jac;
   } else {  // vertex (quadrature.cpp:151-177)
     const double t = gx[i1];
-    const double v1 = t * gx[i2], v2 = t * gx[i3], v3 = t * gx[i4];
+    const double v1 = t * gx[i2], v2 = t * gx[i3];
+    for (int k = 0; k < 4; ++k) c1[k] = 0.0;
     switch (sec) {
-      case 0: ua = t; va = v1; ub = v2; vb = v3; break;
-      case 1: ua = v1; va = t; ub = v2; vb = v3; break;
-      case 2: ua = v1; va = v2; ub = t; vb = v3; break;
-      default: ua = v1; va = v2; ub = v3; vb = t; break;
+      case 0: c0[0] = t;  c0[1] = v1; c0[2] = v2; c0[3] = 0.0; c1[3] = t; break;
+      case 1: c0[0] = v1; c0[1] = t;  c0[2] = v2; c0[3] = 0.0; c1[3] = t; break;
+      case 2: c0[0] = v1; c0[1] = v2; c0[2] = t;  c0[3] = 0.0; c1[3] = t; break;
+      default: c0[0] = v1; c0[1] = v2; c0[2] = 0.0; c1[2] = t; c0[3] = t; break;
     }
-    w = wp * t * t * t;
+    wl = w3 * t * t * t;
   }
-}
-__device__ __forceinline__ void apply_map(int bits, double& u, double& v) {  // quadrature.hpp:25-29
-  if (bits & 1) {
-    const double t = u;
-    u = v;
-    v = t;
-  }
-  if (bits & 2) u = 1.0 - u;
-  if (bits & 4) v = 1.0 - v;
+  // element maps on the affine forms: swap u/v, then reflect u and/or v
+  auto map2 = [](int bits, double& a0, double& a1, double& b0, double& b1) {
+    if (bits & 1) {
+      double t0 = a0, t1 = a1;
+      a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+    }
+    if (bits & 2) { a0 = 1.0 - a0; a1 = -a1; }
+    if (bits & 4) { b0 = 1.0 - b0; b1 = -b1; }
+  };
+  map2(ma, c0[0], c1[0], c0[1], c1[1]);
+  map2(mb, c0[2], c1[2], c0[3], c1[3]);
 }
 
 struct SingArgs {
@@ -309,13 +378,24 @@ struct SingLayout {
   static constexpr int STAGE = CH * STR * (SW + 1);
   static constexpr int RED = SL * NL * NL * SW;
   static constexpr int BODY = STAGE > RED ? STAGE : RED;
-  static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY) * 8;
+  static constexpr int LMAX = 32;               // rule lines per chunk (setup capacity)
+  // real kernels with up to 9 local functions fit 128 registers: 4 CTAs / SM
+#ifndef IGB_SING_MINB
+#define IGB_SING_MINB 4
+#endif
+  static constexpr int MINB = (KT::KIND == 0 && NL <= 9) ? IGB_SING_MINB : 1;
+  // per line: [element][component][A0..4, B0..4] (80), the affine rule
+  // descriptor (c0, c1) x 4 + weight (9); odd stride (the lines of one warp
+  // read distinct banks)
+  static constexpr int LSTRIDE = 2 * 4 * 10 + 9;
+  static constexpr int SETUP = LMAX * LSTRIDE;
+  static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY + SETUP) * 8;
   static_assert(NL % TS == 0, "tile");
   static_assert(NT <= 128, "tiles");
 };
 
 template <class KT, int CLS>
-__global__ void __launch_bounds__(128) k_singular(GeoArgs g, SingArgs A) {
+__global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs g, SingArgs A) {
   using S = typename KT::S;
   using LY = SingLayout<KT>;
   constexpr int NL = KT::NL, NC = KT::NC, CH = LY::CH, TS = LY::TS, NTR = LY::NTR, NT = LY::NT,
@@ -330,6 +410,7 @@ __global__ void __launch_bounds__(128) k_singular(GeoArgs g, SingArgs A) {
   double* body = gw + 64;
   S* Ga = reinterpret_cast<S*>(body);
   double* Fb = body + CH * STR * LY::SW;
+  double* setup = body + LY::BODY;
 
   const int tid = threadIdx.x;
   const int pr = blockIdx.x;
@@ -367,19 +448,53 @@ __global__ void __launch_bounds__(128) k_singular(GeoArgs g, SingArgs A) {
   const int tr = (tile / NTR) * TS, tc = (tile % NTR) * TS;
   const bool active = slice < SL;
 
-  for (int base = 0; base < npts; base += CH) {
-    if (tid < CH) {
-      const int p = base + tid;
+  // chunks of whole rule lines.  Setup: per (line, element, homogeneous
+  // component) the inner Horner sums of the jet at the line's fixed coordinate
+  // (task (e, c) = (0, 0) also stores the line's affine rule descriptor);
+  // then one thread per point finishes both jets from the setup.
+  const int nlines = npts / n;
+  const int lpc = min(LY::LMAX, CH / n), cpts = lpc * n;
+  const float rn = 1.0f / static_cast<float>(n);
+  const int my_ll = div_n(tid, n, rn), my_k = tid - my_ll * n;  // this thread's point of a chunk
+  for (int lbase = 0; lbase < nlines; lbase += lpc) {
+    for (int task = tid; task < lpc * 8; task += 128) {
+      const int ll = task >> 3, e = (task >> 2) & 1, c = task & 3;
+      const int line = lbase + ll;
+      if (line < nlines) {
+        double c0[4], c1[4], wl;
+        rule_line<CLS>(line, n, rn, gx, gw, ma, mb, c0, c1, wl);
+        // the moving parameter of element e is the one with c1 != 0
+        const int vm = e ? (c1[3] != 0.0) : (c1[1] != 0.0);
+        const double sx0 = e ? sxb : sxa, sy0 = e ? syb : sya;
+        const double f = vm ? sx0 + h * c0[2 * e] : sy0 + h * c0[2 * e + 1];
+        double* L = setup + ll * LY::LSTRIDE;
+        jet_setup((e ? cfb : cfa) + c * 25, vm, f, L + (e * 4 + c) * 10);
+        if (task % 8 == 0) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            L[80 + 2 * k] = c0[k];
+            L[81 + 2 * k] = c1[k];
+          }
+          L[88] = wl;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < cpts) {
+      const int p = lbase * n + tid;
       S* ga = Ga + tid * STR;
       double* fb = Fb + tid * STR;
       if (p < npts) {
-        double ua, va, ub, vb, w;
-        rule_point<CLS>(p, n, gx, gw, ua, va, ub, vb, w);
-        apply_map(ma, ua, va);
-        apply_map(mb, ub, vb);
+        const double* L = setup + my_ll * LY::LSTRIDE;
+        const double gk4 = gx[my_k];
+        const double ua = fma(L[81], gk4, L[80]), va = fma(L[83], gk4, L[82]);
+        const double ub = fma(L[85], gk4, L[84]), vb = fma(L[87], gk4, L[86]);
+        const double w = L[88] * gw[my_k];
+        const int vma = L[83] != 0.0, vmb = L[87] != 0.0;
+        const double sa_ = sxa + h * ua, ta_ = sya + h * va, sb_ = sxb + h * ub, tb_ = syb + h * vb;
         double xa[3], dua[3], dva[3], xb[3], dub[3], dvb[3];
-        jet<4>(cfa, sxa + h * ua, sya + h * va, xa, dua, dva);
-        jet<4>(cfb, sxb + h * ub, syb + h * vb, xb, dub, dvb);
+        jet_line(L, vma, vma ? ta_ : sa_, xa, dua, dva);
+        jet_line(L + 40, vmb, vmb ? tb_ : sb_, xb, dub, dvb);
         const double sga = sqrt_g_of(dua, dva), sgb = sqrt_g_of(dub, dvb);
         const double d0 = xa[0] - xb[0], d1 = xa[1] - xb[1], d2 = xa[2] - xb[2];
         const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, g.kp);
@@ -410,7 +525,7 @@ __global__ void __launch_bounds__(128) k_singular(GeoArgs g, SingArgs A) {
     }
     __syncthreads();
     if (active) {
-      for (int pt = slice; pt < CH; pt += SL) {
+      for (int pt = slice; pt < cpts; pt += SL) {
         const S* ga = Ga + pt * STR;
         const double* fb = Fb + pt * STR;
 #pragma unroll
