@@ -18,6 +18,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 
 #include "igb_device.hpp"
 
@@ -597,15 +598,17 @@ __global__ void k_coef(int n, const S* __restrict__ x, const int* __restrict__ l
 }
 __device__ __forceinline__ double operator_mul(double a, double b) { return a * b; }
 
-template <class S>
-__global__ void k_leaf_up(int n_el, const int* __restrict__ el, int nl, int rows, int epp, int npp, int leaf_off,
+template <class S, int NL>
+__global__ void k_leaf_up(int n_el, const int* __restrict__ el, int rows, int epp, int npp, int leaf_off,
                           const double* __restrict__ mom, const S* __restrict__ coef,
                           S* __restrict__ up) {  // h2.cpp:281-290, owned leaves
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n_el) * rows) return;
   const int e = el[idx / rows], r = static_cast<int>(idx % rows);
   S acc = zero<S>();
-  for (int l = 0; l < nl; ++l) fmac(acc, coef[static_cast<size_t>(e) * nl + l], mom[(static_cast<size_t>(e) * nl + l) * rows + r]);
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+    fmac(acc, coef[static_cast<size_t>(e) * NL + l], __ldg(mom + (static_cast<size_t>(e) * NL + l) * rows + r));
   const int leaf = (e / epp) * npp + leaf_off + (e % epp);
   up[static_cast<size_t>(leaf) * rows + r] = acc;
 }
@@ -620,11 +623,14 @@ __device__ __forceinline__ void cluster_node(int c, int level, int sc, int& p, i
 }
 
 // parent(i,j) = sum_k tu_k X_k tv_k^T  (h2.cpp:291-310); level 0: all roots,
-// level >= 1: the nodes of level-1 clusters [c0, c1)
-template <class S>
-__global__ void k_up_level(int np, int level, int npp, int off_l, int off_c, int m, int nch,
+// level >= 1: the nodes of level-1 clusters [c0, c1).  M > 0: compile-time
+// interpolation degree (loops unrolled, all child loads in flight at once);
+// M = 0: runtime m.
+template <class S, int M>
+__global__ void k_up_level(int np, int level, int npp, int off_l, int off_c, int m_rt, int nch,
                            const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ up, int c0,
                            int c1) {
+  const int m = M ? M : m_rt;
   const int mm = m * m, rows = nch * mm, nside = 1 << level;
   const int per = level == 0 ? 1 : (1 << (2 * (level - 1)));
   const int ncl = level == 0 ? np : (c1 - c0);
@@ -643,15 +649,18 @@ __global__ void k_up_level(int np, int level, int npp, int off_l, int off_c, int
   const int c = r / mm, nu = r % mm, i = nu % m, j = nu / m;
   const int cside = nside * 2;
   S acc = zero<S>();
+#pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int child = p * npp + off_c + (2 * sx + (k & 1)) + cside * (2 * sy + (k >> 1));
     const double* tu = (k & 1) ? tr : tl;
     const double* tv = (k >> 1) ? tr : tl;
     const S* X = up + static_cast<size_t>(child) * rows + c * mm;
+#pragma unroll
     for (int b = 0; b < m; ++b) {
       S t = zero<S>();
-      for (int a = 0; a < m; ++a) fmac(t, X[a + m * b], tu[i + m * a]);
-      fmac(acc, t, tv[j + m * b]);
+#pragma unroll
+      for (int a = 0; a < m; ++a) fmac(t, X[a + m * b], __ldg(tu + i + m * a));
+      fmac(acc, t, __ldg(tv + j + m * b));
     }
   }
   up[static_cast<size_t>(p * npp + off_l + sx + nside * sy) * rows + r] = acc;
@@ -1003,12 +1012,13 @@ __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs,
 }
 
 // child(i,j) += tu^T X tv  (h2.cpp:328-347): children at level+1 >= 1 in
-// level-1 clusters [c0, c1)
-template <class S>
-__global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, int m, int nch,
+// level-1 clusters [c0, c1); M as in k_up_level
+template <class S, int M>
+__global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, int m_rt, int nch,
                              const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ down,
                              int c0, int c1) {
   (void)np;
+  const int m = M ? M : m_rt;
   const int mm = m * m, rows = nch * mm, cside = 2 << level, per = 1 << (2 * level);
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(c1 - c0) * per * rows) return;
@@ -1022,10 +1032,12 @@ __global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, i
   const double* tv = (sy & 1) ? tr : tl;
   const S* X = down + static_cast<size_t>(parent) * rows + c * mm;
   S acc = zero<S>();
+#pragma unroll
   for (int b = 0; b < m; ++b) {
     S t = zero<S>();
-    for (int a = 0; a < m; ++a) fmac(t, X[a + m * b], tu[a + m * i]);
-    fmac(acc, t, tv[b + m * j]);
+#pragma unroll
+    for (int a = 0; a < m; ++a) fmac(t, X[a + m * b], __ldg(tu + a + m * i));
+    fmac(acc, t, __ldg(tv + b + m * j));
   }
   S* Y = down + static_cast<size_t>(p * npp + off_c + sx + cside * sy) * rows + c * mm;
   Y[nu] = Y[nu] + acc;
@@ -1088,26 +1100,24 @@ __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict
   }
 }
 
-// leaf backward transform moments^T down + near rows (h2.cpp:359-371); one warp per element
+// leaf backward transform moments^T down + near rows (h2.cpp:359-371); one
+// thread per (owned element, local function)
 template <class S, int NL>
 __global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restrict__ el, int rows, int epp, int npp,
                                                    int leaf_off, const double* __restrict__ mom,
                                                    const S* __restrict__ down, const S* __restrict__ near_rows,
                                                    S* __restrict__ loc) {
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= n_el) return;
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n_el) * NL) return;
+  const int i = static_cast<int>(idx / NL), l = static_cast<int>(idx % NL);
   const int e = el[i];
   const int leaf = (e / epp) * npp + leaf_off + (e % epp);
   const S* dn = down + static_cast<size_t>(leaf) * rows;
-#pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    S s = zero<S>();
-    const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
-    for (int r = lane; r < rows; r += 32) fmac(s, dn[r], mc[r]);
-    const S b = warp_sum(s);
-    if (lane == 0) loc[static_cast<size_t>(i) * NL + l] = near_rows[static_cast<size_t>(i) * NL + l] + b;
-  }
+  const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
+  S acc = zero<S>();
+#pragma unroll 8
+  for (int r = 0; r < rows; ++r) fmac(acc, dn[r], __ldg(mc + r));
+  loc[idx] = near_rows[idx] + acc;
 }
 
 template <class S>
@@ -1133,6 +1143,36 @@ __global__ void k_zero(size_t n, S* p) {
 
 // ====================================================== host driver
 using namespace dev;
+
+// transfer kernels with the interpolation degree as a template parameter
+template <class S, class... A>
+static void launch_up_level(unsigned grid, cudaStream_t s, A... a) {
+  const int m = std::get<5>(std::make_tuple(a...));
+  switch (m) {
+    case 2: k_up_level<S, 2><<<grid, 256, 0, s>>>(a...); break;
+    case 3: k_up_level<S, 3><<<grid, 256, 0, s>>>(a...); break;
+    case 4: k_up_level<S, 4><<<grid, 256, 0, s>>>(a...); break;
+    case 5: k_up_level<S, 5><<<grid, 256, 0, s>>>(a...); break;
+    case 6: k_up_level<S, 6><<<grid, 256, 0, s>>>(a...); break;
+    case 7: k_up_level<S, 7><<<grid, 256, 0, s>>>(a...); break;
+    case 8: k_up_level<S, 8><<<grid, 256, 0, s>>>(a...); break;
+    default: k_up_level<S, 0><<<grid, 256, 0, s>>>(a...); break;
+  }
+}
+template <class S, class... A>
+static void launch_down_level(unsigned grid, cudaStream_t s, A... a) {
+  const int m = std::get<5>(std::make_tuple(a...));
+  switch (m) {
+    case 2: k_down_level<S, 2><<<grid, 256, 0, s>>>(a...); break;
+    case 3: k_down_level<S, 3><<<grid, 256, 0, s>>>(a...); break;
+    case 4: k_down_level<S, 4><<<grid, 256, 0, s>>>(a...); break;
+    case 5: k_down_level<S, 5><<<grid, 256, 0, s>>>(a...); break;
+    case 6: k_down_level<S, 6><<<grid, 256, 0, s>>>(a...); break;
+    case 7: k_down_level<S, 7><<<grid, 256, 0, s>>>(a...); break;
+    case 8: k_down_level<S, 8><<<grid, 256, 0, s>>>(a...); break;
+    default: k_down_level<S, 0><<<grid, 256, 0, s>>>(a...); break;
+  }
+}
 
 // Device memory comes from one stream-ordered pool per device that keeps
 // freed memory reserved (release threshold = max): operators built and
@@ -1701,14 +1741,14 @@ void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, c
     ++launches;
     IGB_CUDA(cudaEventRecord(ev_join_, side_));
   }
-  k_leaf_up<S><<<grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s>>>(
-      nel, d_el_, NL, rows, epp, npp, P.level_offset[L], d_mom_, coef, up);
+  k_leaf_up<S, NL><<<grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s>>>(
+      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, coef, up);
   ++launches;
   mark(2);
   for (int l = L - 1; l >= 1; --l) {
     const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * (l - 1))) * rows;
-    k_up_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
-                                                      d_tl_, d_tr_, up, Lp.c0, Lp.c1);
+    launch_up_level<S>(grid_for(tot, 256), s, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                       d_tl_, d_tr_, up, Lp.c0, Lp.c1);
     ++launches;
   }
   if (Lp.world > 1 && Lp.pack_nodes.size()) {
@@ -1749,8 +1789,8 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
   }
   if (L >= 1) {  // roots (replicated on every rank)
     const long long tot = static_cast<long long>(np) * rows;
-    k_up_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, 0, npp, P.level_offset[0], P.level_offset[1], m, nch_,
-                                                      d_tl_, d_tr_, up, 0, 0);
+    launch_up_level<S>(grid_for(tot, 256), s, np, 0, npp, P.level_offset[0], P.level_offset[1], m, nch_, d_tl_,
+                       d_tr_, up, 0, 0);
     ++launches;
   }
   mark(3);
@@ -1822,21 +1862,20 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
     ++launches;
   }
   mark(5);
-  for (int l = 0; l < L; ++l) {
-    const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
-    k_down_level<S><<<grid_for(tot, 256), 256, 0, s>>>(np, l, npp, P.level_offset[l], P.level_offset[l + 1], m,
-                                                        nch_, d_tl_, d_tr_, down, Lp.c0, Lp.c1);
-    ++launches;
-  }
-  mark(6);
-  if (pev == nullptr) {
-    IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
-  } else {
+  if (pev != nullptr) {  // profiling: the near rows serialised as their own phase
     k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s>>>(
         nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
     ++launches;
   }
-  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s>>>(
+  mark(6);
+  for (int l = 0; l < L; ++l) {
+    const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
+    launch_down_level<S>(grid_for(tot, 256), s, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                         d_tl_, d_tr_, down, Lp.c0, Lp.c1);
+    ++launches;
+  }
+  if (pev == nullptr) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));  // near rows (side stream) done
+  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s>>>(
       nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
   ++launches;
   mark(7);

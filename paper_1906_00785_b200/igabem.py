@@ -555,7 +555,10 @@ class H2Matrix:
         _check(lib().igb_h2_reassemble(self._h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
 
-    PHASES = ("coef", "leaf_up", "upward", "zero", "far", "downward", "near_leaf", "scatter")
+    # profile_apply phases (serialised, CUDA events): near_rows = near-field
+    # rows (overlapped with the far field in the graph), downward = downward
+    # pass + leaf backward transform
+    PHASES = ("coef", "leaf_up", "upward", "zero", "far", "near_rows", "downward", "scatter")
 
     def profile_apply(self, iters=10):
         """Per-phase matvec device time (ms, summed over iters)."""
