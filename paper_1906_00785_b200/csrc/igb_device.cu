@@ -997,6 +997,9 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
 
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
 // in ascending t (fixed order)
+// (single GPU: every pair slot was written -- unconditional, unrolled stream
+// over the row's contiguous slots; multi-GPU: only pairs with an owned source)
+template <bool DIST>
 __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs, const int* __restrict__ upper_start,
                             const int* __restrict__ far_b, const unsigned char* __restrict__ owned,
                             const double* __restrict__ slot, double* __restrict__ down) {
@@ -1004,10 +1007,16 @@ __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs,
   if (idx >= static_cast<long long>(n_nodes) * mm) return;
   const int s = static_cast<int>(idx / mm), nu = static_cast<int>(idx % mm);
   const int q0 = far_rs[s], q1 = upper_start[s];
-  if (q0 == q1 || !owned[s]) return;
+  if (q0 == q1 || (DIST && !owned[s])) return;
   double acc = down[idx];
-  for (int q = q0; q < q1; ++q)
-    if (owned[far_b[q]]) acc += slot[static_cast<size_t>(q) * mm + nu];
+  const double* sp = slot + static_cast<size_t>(q0) * mm + nu;
+  if constexpr (DIST) {
+    for (int q = q0; q < q1; ++q, sp += mm)
+      if (owned[far_b[q]]) acc += *sp;
+  } else {
+#pragma unroll 8
+    for (int q = q0; q < q1; ++q, sp += mm) acc += __ldcs(sp);  // read once: streaming
+  }
   down[idx] = acc;
 }
 
@@ -1840,7 +1849,12 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
       }
 #undef IGB_FS
       ++launches;
-      k_far_lower<<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn);
+      if (lp_.world > 1)
+        k_far_lower<true><<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(
+            P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn);
+      else
+        k_far_lower<false><<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(
+            P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn);
     } else {
       KParams kp;
       kp.kr = as_.kp[0];
