@@ -999,13 +999,16 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
 // in ascending t (fixed order)
 // (single GPU: every pair slot was written -- unconditional, unrolled stream
 // over the row's contiguous slots; multi-GPU: only pairs with an owned source)
+// rows: 0 all, 1 leaf-level rows only, 2 the other levels (level-split graph)
 template <bool DIST>
 __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs, const int* __restrict__ upper_start,
                             const int* __restrict__ far_b, const unsigned char* __restrict__ owned,
-                            const double* __restrict__ slot, double* __restrict__ down) {
+                            const double* __restrict__ slot, double* __restrict__ down, int rows = 0, int npp = 1,
+                            int leaf_off = 0) {
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n_nodes) * mm) return;
   const int s = static_cast<int>(idx / mm), nu = static_cast<int>(idx % mm);
+  if (rows != 0 && ((s % npp >= leaf_off) != (rows == 1))) return;
   const int q0 = far_rs[s], q1 = upper_start[s];
   if (q0 == q1 || (DIST && !owned[s])) return;
   double acc = down[idx];
@@ -1315,7 +1318,10 @@ H2Device::~H2Device() {
   pinned_put(h_y_pinned_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  if (ev_fork2_) cudaEventDestroy(ev_fork2_);
+  if (ev_join2_) cudaEventDestroy(ev_join2_);
   if (side_) cudaStreamDestroy(side_);
+  if (side2_) cudaStreamDestroy(side2_);
   if (aux_) cudaStreamDestroy(aux_);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -1400,8 +1406,11 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   d_loc_ = dalloc<double>(Lp.el.size() * NL * sw);
   d_nrows_ = dalloc<double>(Lp.el.size() * NL * sw);
   IGB_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  IGB_CUDA(cudaStreamCreateWithFlags(&side2_, cudaStreamNonBlocking));
   IGB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   IGB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  IGB_CUDA(cudaEventCreateWithFlags(&ev_fork2_, cudaEventDisableTiming));
+  IGB_CUDA(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
   IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1537,6 +1546,12 @@ void H2Device::stage_plan() {
         if (Lp.world > 1 || P.far_upper_start[t] < P.far_row_start[t + 1]) sym_targets.push_back(t);
       n_sym_targets_ = static_cast<int>(sym_targets.size());
       d_sym_targets_ = upload(sym_targets);
+      std::vector<int> fine, coarse;
+      for (int t : sym_targets) (P.node_level[t] == P.depth ? fine : coarse).push_back(t);
+      n_sym_fine_ = static_cast<int>(fine.size());
+      n_sym_coarse_ = static_cast<int>(coarse.size());
+      d_sym_fine_ = upload(fine);
+      d_sym_coarse_ = upload(coarse);
       d_upper_start_ = upload(P.far_upper_start);
       d_trans_ = upload(P.far_trans);
       d_slot_ = dalloc<double>(P.far_a.size() * static_cast<size_t>(mm));
@@ -1907,6 +1922,100 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
   apply_launches_ = launches;
 }
 
+// Single-GPU matvec graph split by tree level (symmetric far field).  Far pairs
+// join clusters of one level, and most of them sit on the leaf level, which
+// only needs the leaf moments.  Main stream: coefficients, leaf moments, zero,
+// leaf-level far field + its transposed slots, last downward level, leaf
+// transform, gather.  Side stream 2, concurrently: upward pass, coarse-level
+// far field + slots, downward levels above the leaves.  Side stream 1: near rows.
+template <class KT>
+void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t s) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL;
+  const Discretization& d = *disc_;
+  const H2Plan& P = plan_;
+  const LocalPlan& Lp = lp_;
+  const int m = P.m, mm = m * m, rows = nch_ * mm, L = P.depth;
+  const int np = P.n_patches, npp = P.npp, epp = d.elements_per_patch();
+  const int nel = static_cast<int>(Lp.el.size()), nloc = d.element_count() * NL;
+  const S* x = reinterpret_cast<const S*>(xin);
+  S* y = reinterpret_cast<S*>(yout);
+  S* coef = reinterpret_cast<S*>(d_coef_);
+  S* up = reinterpret_cast<S*>(d_up_);
+  S* down = reinterpret_cast<S*>(d_down_);
+  S* loc = reinterpret_cast<S*>(d_loc_);
+  S* nrows = reinterpret_cast<S*>(d_nrows_);
+  double* dn = reinterpret_cast<double*>(down);
+  const double* upd = reinterpret_cast<const double*>(up);
+  int launches = 0;
+  k_coef<S><<<grid_for(nloc, 256), 256, 0, s>>>(nloc, x, d_l2g_, d_lsign_, coef);
+  ++launches;
+  IGB_CUDA(cudaEventRecord(ev_fork_, s));
+  IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+  k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
+      nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
+  ++launches;
+  IGB_CUDA(cudaEventRecord(ev_join_, side_));
+  k_leaf_up<S, NL><<<grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s>>>(
+      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, coef, up);
+  const size_t ndown = static_cast<size_t>(P.n_nodes) * rows;
+  k_zero<S><<<grid_for(static_cast<long long>(ndown), 256), 256, 0, s>>>(ndown, down);
+  launches += 2;
+  IGB_CUDA(cudaEventRecord(ev_fork2_, s));
+  IGB_CUDA(cudaStreamWaitEvent(side2_, ev_fork2_, 0));
+  auto far_sym = [&](cudaStream_t st, int n, const int* targets) {
+    if (n == 0) return;
+    const unsigned g = grid_for(static_cast<long long>(n) * 32, 256);
+    switch (m) {
+      case 2: k_far_sym<2, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
+      case 3: k_far_sym<3, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
+      case 4: k_far_sym<4, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
+      case 5: k_far_sym<5, false, 1><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
+      default: k_far_sym<6, false, 1><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
+    }
+    ++launches;
+  };
+  auto far_lower = [&](cudaStream_t st, int which) {
+    k_far_lower<false><<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, st>>>(
+        P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn, which, npp, P.level_offset[L]);
+    ++launches;
+  };
+  // side stream 2: upward pass, coarse far field, downward levels 0 .. L-2
+  for (int l = L - 1; l >= 0; --l) {
+    const long long tot = (l == 0 ? static_cast<long long>(np) : static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * (l - 1)))) * rows;
+    launch_up_level<S>(grid_for(tot, 256), side2_, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                       d_tl_, d_tr_, up, l == 0 ? 0 : Lp.c0, l == 0 ? 0 : Lp.c1);
+    ++launches;
+  }
+  far_sym(side2_, n_sym_coarse_, d_sym_coarse_);
+  far_lower(side2_, 2);
+  for (int l = 0; l + 1 < L; ++l) {
+    const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
+    launch_down_level<S>(grid_for(tot, 256), side2_, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                         d_tl_, d_tr_, down, Lp.c0, Lp.c1);
+    ++launches;
+  }
+  IGB_CUDA(cudaEventRecord(ev_join2_, side2_));
+  // main: leaf-level far field
+  far_sym(s, n_sym_fine_, d_sym_fine_);
+  far_lower(s, 1);
+  IGB_CUDA(cudaStreamWaitEvent(s, ev_join2_, 0));
+  {
+    const int l = L - 1;
+    const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
+    launch_down_level<S>(grid_for(tot, 256), s, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                         d_tl_, d_tr_, down, Lp.c0, Lp.c1);
+    ++launches;
+  }
+  IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s>>>(
+      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
+  k_scatter<S><<<grid_for(d.dof_count(), 256), 256, 0, s>>>(d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
+  launches += 2;
+  IGB_CUDA(cudaGetLastError());
+  apply_launches_ = launches;
+}
+
 template <class F>
 void H2Device::dispatch_kind(F&& f) {
   const int kind = disc_->kind();
@@ -1982,7 +2091,12 @@ void H2Device::launch_apply_graph(cudaStream_t s) {
   if (!graph_exec_) {
     cudaGraph_t graph;
     IGB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-    enqueue_apply_dispatch(dx_, dy_, stream_, nullptr);
+    if (split_graph())
+      dispatch_kind([&](auto kt) {
+        if constexpr (decltype(kt)::KIND == 0) enqueue_apply_split<decltype(kt)>(dx_, dy_, stream_);
+      });
+    else
+      enqueue_apply_dispatch(dx_, dy_, stream_, nullptr);
     IGB_CUDA(cudaStreamEndCapture(stream_, &graph));
     IGB_CUDA(cudaGraphInstantiate(&graph_exec_, graph, 0));
     cudaGraphDestroy(graph);

@@ -89,6 +89,9 @@ class H2Device {
   enum { kEvStart, kEvElements, kEvCoincident, kEvEdge, kEvVertex, kEvUploaded, kEvPlanPhase, kEvImages,
          kEvCouplings, kEvRegular, kEvScatter, kAsmEvents };
   template <class KT> void enqueue_apply(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev);
+  template <class KT> void enqueue_apply_split(const double* x, double* y, cudaStream_t s);
+  // the single-GPU symmetric far field is captured as the level-split graph
+  bool split_graph() const { return sym_far_ && lp_.world == 1 && plan_.depth >= 1; }
   template <class KT> void enqueue_phase1(const double* x, double* send, cudaStream_t s, cudaEvent_t* pev, int& n);
   template <class KT> void enqueue_phase2(const double* recv, double* y, cudaStream_t s, cudaEvent_t* pev, int& n);
   template <class F> void dispatch_kind(F&& f);
@@ -134,6 +137,8 @@ class H2Device {
   bool sym_far_ = false;
   int n_sym_targets_ = 0;
   int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;
+  int n_sym_fine_ = 0, n_sym_coarse_ = 0;  // leaf-level / coarser symmetric targets
+  int *d_sym_fine_ = nullptr, *d_sym_coarse_ = nullptr;
   double* d_slot_ = nullptr;
   int *d_far_a_ = nullptr;
   int *d_dof_start_ = nullptr, *d_dof_inc_ = nullptr;
@@ -153,8 +158,8 @@ class H2Device {
          *d_loc_ = nullptr;
   double *h_x_pinned_ = nullptr, *h_y_pinned_ = nullptr;
   double* d_nrows_ = nullptr;
-  cudaStream_t side_ = nullptr;
-  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  cudaStream_t side_ = nullptr, side2_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_fork2_ = nullptr, ev_join2_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   int apply_launches_ = 0, phase1_launches_ = 0;
   int assembly_kernels_ = 0, assembly_launches_count_ = 0;
