@@ -41,13 +41,21 @@ CONFIGS = {
 FP64_PEAK_TFLOPS = 36.85  # DFMA microbenchmark on this pool's B200 (profiles/r01_fp64_peak_probe.txt)
 
 
+class _Traffic(dict):
+    def get(self, prefix, default=None):  # kernel names carry template arguments: match by prefix
+        for k, v in self.items():
+            if k == prefix or k.startswith(prefix.rstrip(">") + ",") or k.startswith(prefix):
+                return v
+        return default
+
+
 def load_traffic():
     """per-launch DRAM bytes of the dominant kernels from the committed ncu capture"""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic_c2.json")) as f:
-            return json.load(f)["kernels"]
+            return _Traffic(json.load(f)["kernels"])
     except Exception:
-        return {}
+        return _Traffic()
 
 
 def load_peaks():

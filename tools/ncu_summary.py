@@ -66,8 +66,8 @@ def full(path, traffic):
         k = short(r[ki])
         if traffic is not None and k not in traffic:
             g = lambda m: float(r[hdr.index(m)].replace(",", "")) * scale.get(units[hdr.index(m)], 1)
-            traffic[k] = {"time_us": float(r[hdr.index("gpu__time_duration.sum")].replace(",", "")) *
-                          (1e-3 if units[hdr.index("gpu__time_duration.sum")] == "nsecond" else 1.0),
+            ti = hdr.index("gpu__time_duration.sum")
+            traffic[k] = {"time_us": float(r[ti].replace(",", "")) * UNITS.get(units[ti], 1.0) * 1e3,
                           "dram_read_bytes": g("dram__bytes_read.sum"), "dram_write_bytes": g("dram__bytes_write.sum")}
     print()
 
