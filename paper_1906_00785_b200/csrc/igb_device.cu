@@ -10,6 +10,7 @@
 // are bitwise reproducible run to run.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -170,8 +171,13 @@ __global__ void __launch_bounds__(256) k_couplings(long long n_pairs, int mm, co
 
 // --------------------------------------------------- K4: regular near
 // blk = sum_c w_c A_c^T (K B_c)  (pair_integration.hpp:76-95)
+// Regular near blocks (pair_integration.hpp far_block 76-95): tensor Gauss on
+// both elements from the element caches.  One CTA integrates P unique pairs
+// (ea < eb); the block goes to the slot of (ea, eb) and its transpose to the
+// slot of (eb, ea) (either may be another rank's, -1).
 template <class KT>
-__global__ void __launch_bounds__(128) k_regular(const int* __restrict__ slots, const int* __restrict__ near_a,
+__global__ void __launch_bounds__(128) k_regular(int n_pairs, int P, const int* __restrict__ slot_ab,
+                                                 const int* __restrict__ slot_ba, const int* __restrict__ near_a,
                                                  const int* __restrict__ near_b, const int* __restrict__ near_rs,
                                                  const int* __restrict__ near_ea, int nq,
                                                  const double* __restrict__ cpts, const double* __restrict__ cval,
@@ -179,13 +185,25 @@ __global__ void __launch_bounds__(128) k_regular(const int* __restrict__ slots, 
   using S = typename KT::S;
   constexpr int NL = KT::NL, NC = KT::NC;
   extern __shared__ __align__(16) double sm[];
-  S* KB = reinterpret_cast<S*>(sm);  // [NC][nq][NL]
-  const int q = slots[blockIdx.x];
-  const int ea = near_ea[q], eb = near_b[q];
-  const double* pa = cpts + static_cast<size_t>(ea) * nq * 3;
-  const double* pb = cpts + static_cast<size_t>(eb) * nq * 3;
-  for (int it = threadIdx.x; it < nq * NC; it += blockDim.x) {
-    const int i = it % nq, c = it / nq;
+  S* KB = reinterpret_cast<S*>(sm);  // [P][NC][nq][NL]
+  const int p0 = blockIdx.x * P, np = min(P, n_pairs - p0);
+  auto elems = [&](int p, int& ea, int& eb) {
+    const int qab = slot_ab[p0 + p];
+    if (qab >= 0) {
+      ea = near_ea[qab];
+      eb = near_b[qab];
+    } else {
+      const int qba = slot_ba[p0 + p];
+      ea = near_b[qba];
+      eb = near_ea[qba];
+    }
+  };
+  for (int it = threadIdx.x; it < np * NC * nq; it += blockDim.x) {
+    const int p = it / (NC * nq), r = it % (NC * nq), c = r / nq, i = r % nq;
+    int ea, eb;
+    elems(p, ea, eb);
+    const double* pa = cpts + static_cast<size_t>(ea) * nq * 3;
+    const double* pb = cpts + static_cast<size_t>(eb) * nq * 3;
     const double xa = pa[3 * i], ya = pa[3 * i + 1], za = pa[3 * i + 2];
     const double* B = cval + (static_cast<size_t>(eb) * NC + c) * nq * NL;
     S acc[NL];
@@ -198,24 +216,28 @@ __global__ void __launch_bounds__(128) k_regular(const int* __restrict__ slots, 
       for (int l = 0; l < NL; ++l) fmac(acc[l], gk, B[j * NL + l]);
     }
 #pragma unroll
-    for (int l = 0; l < NL; ++l) KB[(c * nq + i) * NL + l] = acc[l];
+    for (int l = 0; l < NL; ++l) KB[((p * NC + c) * nq + i) * NL + l] = acc[l];
   }
   __syncthreads();
   S* out = reinterpret_cast<S*>(near);
-  for (int o = threadIdx.x; o < NL * NL; o += blockDim.x) {
-    const int la = o / NL, lb = o % NL;
+  for (int o = threadIdx.x; o < np * NL * NL; o += blockDim.x) {
+    const int p = o / (NL * NL), la = (o / NL) % NL, lb = o % NL;
+    int ea, eb;
+    elems(p, ea, eb);
     S tot = zero<S>();
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const double* A = cval + (static_cast<size_t>(ea) * NC + c) * nq * NL;
       S s = zero<S>();
-      for (int i = 0; i < nq; ++i) fmac(s, KB[(c * nq + i) * NL + lb], A[i * NL + la]);
+      for (int i = 0; i < nq; ++i) fmac(s, KB[((p * NC + c) * nq + i) * NL + lb], A[i * NL + la]);
       if constexpr (KT::KIND == 2) {
         if (c == 3) s = s * mk(kp.dwx, kp.dwy);
       }
       tot = tot + s;
     }
-    out[near_off(near_a, near_rs, q, la, lb, NL)] = tot;
+    const int qab = slot_ab[p0 + p], qba = slot_ba[p0 + p];
+    if (qab >= 0) out[near_off(near_a, near_rs, qab, la, lb, NL)] = tot;
+    if (qba >= 0) out[near_off(near_a, near_rs, qba, lb, la, NL)] = tot;
   }
 }
 
@@ -1569,7 +1591,8 @@ void H2Device::stage_plan() {
     as_.sing[c][2] = upload(Lp.sing[c].slot_ab);
     as_.sing[c][3] = upload(Lp.sing[c].slot_ba);
   }
-  as_.reg = upload(Lp.reg_slot);
+  as_.reg = upload(Lp.reg_ab);
+  as_.reg_ba = upload(Lp.reg_ba);
   const long long nnear = static_cast<long long>(Lp.near_row.size());
   const long long nfarp = static_cast<long long>(P.far_a.size());
   d_near_ = dalloc<double>(static_cast<size_t>(nnear) * NL * NL * sw);
@@ -1667,12 +1690,15 @@ void H2Device::launch_plan_phase(cudaEvent_t* ev, int& launched) {
     IGB_CUDA(cudaGetLastError());
   }
   IGB_CUDA(cudaEventRecord(ev[kEvCouplings], stream_));
-  if (!lp_.reg_slot.empty()) {
-    const size_t smem = static_cast<size_t>(NC) * nq * NL * 8 * sw;
+  if (!lp_.reg_ab.empty()) {
+    const int npair = static_cast<int>(lp_.reg_ab.size());
+    const int per = std::max(1, 128 / (NC * nq));  // pairs per CTA: one work item per thread
+    const size_t smem = static_cast<size_t>(per) * NC * nq * NL * 8 * sw;
     IGB_CUDA(cudaFuncSetAttribute(k_regular<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     if (smem > 200 * 1024) throw std::invalid_argument("B200 H2: far quadrature order too large");
-    k_regular<KT><<<static_cast<unsigned>(lp_.reg_slot.size()), 128, smem, stream_>>>(
-        as_.reg, d_near_a_, d_near_b_, d_near_rs_, d_near_ea_, nq, d_cpts_, d_cval_, g.kp, d_near_);
+    k_regular<KT><<<static_cast<unsigned>((npair + per - 1) / per), 128, smem, stream_>>>(
+        npair, per, as_.reg, as_.reg_ba, d_near_a_, d_near_b_, d_near_rs_, d_near_ea_, nq, d_cpts_, d_cval_, g.kp,
+        d_near_);
     ++launched;
     IGB_CUDA(cudaGetLastError());
   }

@@ -167,7 +167,7 @@ class H2Device {
   double alloc_ms_ = 0;
   struct AsmState {
     double *gxf = nullptr, *gwf = nullptr, *gxs = nullptr, *gws = nullptr, *lag = nullptr, *cheb = nullptr;
-    int *reg = nullptr, *node_patch = nullptr, *node_level = nullptr, *node_sx = nullptr, *node_sy = nullptr;
+    int *reg = nullptr, *reg_ba = nullptr, *node_patch = nullptr, *node_level = nullptr, *node_sx = nullptr, *node_sy = nullptr;
     int* sing[4][4] = {};
     unsigned char* singm[4][2] = {};
     double kp[4] = {0, 0, 0, 0};

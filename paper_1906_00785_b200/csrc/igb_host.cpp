@@ -1306,6 +1306,30 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
     L2.slot_ba[i] = sba;
   }
   if (missing) throw std::logic_error("B200 H2: near relation is not symmetric");
+  // unique regular pairs (ea < eb) with both ordered slots: the block of (eb, ea)
+  // is the transpose of (ea, eb) (tensor Gauss rule on both elements, symmetric
+  // kernel), so the device integrates each pair once
+  {
+    const long long nreg = static_cast<long long>(P.reg_slot.size());
+    std::vector<long long> rpos(nreg + 1, 0);
+    for (long long i = 0; i < nreg; ++i) {
+      const int q = P.reg_slot[i];
+      rpos[i + 1] = rpos[i] + (P.near_a[q] < P.near_b[q] ? 1 : 0);
+    }
+    P.reg_ab.resize(rpos[nreg]);
+    P.reg_ba.resize(rpos[nreg]);
+    int miss = 0;
+#pragma omp parallel for schedule(static) reduction(+ : miss)
+    for (long long i = 0; i < nreg; ++i) {
+      const int q = P.reg_slot[i];
+      if (P.near_a[q] >= P.near_b[q]) continue;
+      const int qb = find_slot(P.near_b[q], P.near_a[q]);
+      if (qb < 0) ++miss;
+      P.reg_ab[rpos[i]] = q;
+      P.reg_ba[rpos[i]] = qb;
+    }
+    if (miss) throw std::logic_error("B200 H2: near relation is not symmetric");
+  }
   lap("classify");
   // DOF incidence in ascending (e, l) order (h2.cpp:359-376 scatter order)
   const int nl = d.local_count(), nd = d.dof_count();
@@ -1419,6 +1443,12 @@ LocalPlan build_local_plan(const Discretization& d, const H2Plan& P, int world, 
   }
   for (int q : P.reg_slot)
     if (Lp.slot_local[q] >= 0) Lp.reg_slot.push_back(Lp.slot_local[q]);
+  for (size_t i = 0; i < P.reg_ab.size(); ++i) {
+    const int a = Lp.slot_local[P.reg_ab[i]], b = Lp.slot_local[P.reg_ba[i]];
+    if (a < 0 && b < 0) continue;
+    Lp.reg_ab.push_back(a);
+    Lp.reg_ba.push_back(b);
+  }
   // tree nodes
   Lp.node_owned.assign(nn, 0);
   Lp.rank_pack_nodes.assign(world, {});

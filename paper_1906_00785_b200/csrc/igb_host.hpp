@@ -235,6 +235,7 @@ struct H2Plan {
   using SingList = igb::SingList;
   SingList sing[4];
   std::vector<int> reg_slot;  // regular near pairs (slot into near list)
+  std::vector<int> reg_ab, reg_ba;  // unique regular pairs ea < eb: slots of (ea,eb) and (eb,ea)
   // DOF gather incidence for the deterministic scatter: for dof d the
   // (e*nl + l) entries in ascending order, sign folded in by the device
   std::vector<int> dof_start, dof_inc;
@@ -279,6 +280,7 @@ struct LocalPlan {
   std::vector<int> slot_local;         // global slot -> local slot or -1
   H2Plan::SingList sing[4];            // items touching owned rows; slots local or -1
   std::vector<int> reg_slot;           // local slots of owned regular pairs
+  std::vector<int> reg_ab, reg_ba;     // unique regular pairs touching owned rows: local slots or -1
   std::vector<unsigned char> node_owned;  // per node (roots owned by every rank)
   std::vector<int> far_targets;        // owned nodes with far pairs (ascending)
   std::vector<int> pack_nodes;         // owned nodes at levels >= 1 (ascending): all-gather payload
