@@ -635,6 +635,26 @@ __global__ void k_leaf_up(int n_el, const int* __restrict__ el, int rows, int ep
   up[static_cast<size_t>(leaf) * rows + r] = acc;
 }
 
+// leaf moments straight from x (coefficients gathered inline: h2.cpp:271-290)
+// and, in the same launch, down := 0 (level-split graph)
+template <class S, int NL>
+__global__ void k_leaf_up_x(int n_el, int rows, int epp, int npp, int leaf_off, const double* __restrict__ mom,
+                            const S* __restrict__ x, const int* __restrict__ l2g, const double* __restrict__ sg,
+                            S* __restrict__ up, S* __restrict__ down, long long ndown) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx < ndown) down[idx] = zero<S>();
+  if (idx >= static_cast<long long>(n_el) * rows) return;
+  const int e = static_cast<int>(idx / rows), r = static_cast<int>(idx % rows);
+  S acc = zero<S>();
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const int k = e * NL + l;
+    fmac(acc, x[l2g[k]] * sg[k], __ldg(mom + static_cast<size_t>(k) * rows + r));
+  }
+  const int leaf = (e / epp) * npp + leaf_off + (e % epp);
+  up[static_cast<size_t>(leaf) * rows + r] = acc;
+}
+
 // node of a level-l tree in level-1 cluster c (l >= 1), local index sc
 __device__ __forceinline__ void cluster_node(int c, int level, int sc, int& p, int& sx, int& sy) {
   const int half = 1 << (level - 1);
@@ -1094,10 +1114,17 @@ __global__ void k_unpack(int n, const int* __restrict__ nodes, int rows, const S
 
 // near-field rows per test element (h2.cpp:349-357); one warp per element,
 // streaming its contiguous row [la][k][lb]
-template <class S, int NL>
+// FROM_X: coefficients gathered inline from x (l2g, signs) instead of coef
+template <class S, int NL, bool FROM_X = false>
 __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict__ near_rs,
                                                    const int* __restrict__ near_b, const S* __restrict__ blk,
-                                                   const S* __restrict__ coef, S* __restrict__ rows_out) {
+                                                   const S* __restrict__ coef, S* __restrict__ rows_out,
+                                                   const int* __restrict__ l2g = nullptr,
+                                                   const double* __restrict__ sg = nullptr) {
+  auto cf = [&](int k) -> S {
+    if constexpr (FROM_X) return coef[l2g[k]] * sg[k];
+    else return coef[k];
+  };
   const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (e >= ne) return;
@@ -1114,7 +1141,7 @@ __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int jj = j + 32 * u, k = jj / NL, lb = jj - k * NL;
-      xv[u] = coef[static_cast<size_t>(near_b[rs + k]) * NL + lb];
+      xv[u] = cf(near_b[rs + k] * NL + lb);
     }
 #pragma unroll
     for (int la = 0; la < NL; ++la)
@@ -1123,7 +1150,7 @@ __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict
   }
   for (; j < len; j += 32) {
     const int k = j / NL, lb = j - k * NL;
-    const S xv = coef[static_cast<size_t>(near_b[rs + k]) * NL + lb];
+    const S xv = cf(near_b[rs + k] * NL + lb);
 #pragma unroll
     for (int la = 0; la < NL; ++la) fmac(acc[la], ldg_s(base + static_cast<size_t>(la) * len + j), xv);
   }
@@ -1974,19 +2001,18 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   double* dn = reinterpret_cast<double*>(down);
   const double* upd = reinterpret_cast<const double*>(up);
   int launches = 0;
-  k_coef<S><<<grid_for(nloc, 256), 256, 0, s>>>(nloc, x, d_l2g_, d_lsign_, coef);
-  ++launches;
+  (void)nloc;
+  (void)coef;
   IGB_CUDA(cudaEventRecord(ev_fork_, s));
   IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-  k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
-      nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
+  k_near_rows<S, NL, true><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
+      nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), x, nrows, d_l2g_, d_lsign_);
   ++launches;
   IGB_CUDA(cudaEventRecord(ev_join_, side_));
-  k_leaf_up<S, NL><<<grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s>>>(
-      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, coef, up);
-  const size_t ndown = static_cast<size_t>(P.n_nodes) * rows;
-  k_zero<S><<<grid_for(static_cast<long long>(ndown), 256), 256, 0, s>>>(ndown, down);
-  launches += 2;
+  const long long ndown = static_cast<long long>(P.n_nodes) * rows;
+  k_leaf_up_x<S, NL><<<grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s>>>(
+      nel, rows, epp, npp, P.level_offset[L], d_mom_, x, d_l2g_, d_lsign_, up, down, ndown);
+  ++launches;
   IGB_CUDA(cudaEventRecord(ev_fork2_, s));
   IGB_CUDA(cudaStreamWaitEvent(side2_, ev_fork2_, 0));
   auto far_sym = [&](cudaStream_t st, int n, const int* targets) {
