@@ -64,11 +64,14 @@ def full(path, traffic):
     for r in rows:
         print(f"| `{short(r[ki])[:60]}` | " + " | ".join(r[i] for i, _ in idx) + " |")
         k = short(r[ki])
-        if traffic is not None and k not in traffic:
+        if traffic is not None:  # summed over the captured launches of one kernel (one matvec / one assembly)
             g = lambda m: float(r[hdr.index(m)].replace(",", "")) * scale.get(units[hdr.index(m)], 1)
             ti = hdr.index("gpu__time_duration.sum")
-            traffic[k] = {"time_us": float(r[ti].replace(",", "")) * UNITS.get(units[ti], 1.0) * 1e3,
-                          "dram_read_bytes": g("dram__bytes_read.sum"), "dram_write_bytes": g("dram__bytes_write.sum")}
+            t = traffic.setdefault(k, {"time_us": 0.0, "dram_read_bytes": 0.0, "dram_write_bytes": 0.0, "launches": 0})
+            t["time_us"] += float(r[ti].replace(",", "")) * UNITS.get(units[ti], 1.0) * 1e3
+            t["dram_read_bytes"] += g("dram__bytes_read.sum")
+            t["dram_write_bytes"] += g("dram__bytes_write.sum")
+            t["launches"] += 1
     print()
 
 
@@ -85,4 +88,4 @@ if __name__ == "__main__":
         full(rep, traffic)
     if tpath:
         json.dump({"source": "ncu --set full --clock-control none (tools/gpu_profile.sh, c2 step on B200); per launch, "
-                             "first captured launch of each kernel", "kernels": traffic}, open(tpath, "w"), indent=1)
+                             "summed over the captured launches of each kernel within one matvec (level-split graph: leaf-level + coarse far-field launches) or one assembly", "kernels": traffic}, open(tpath, "w"), indent=1)
