@@ -1362,6 +1362,8 @@ H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, i
 H2Device::~H2Device() {
   cudaSetDevice(device_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph1_) cudaGraphExecDestroy(graph1_);
+  if (graph2_) cudaGraphExecDestroy(graph2_);
   release_memory();
   pinned_put(h_x_pinned_);
   pinned_put(h_y_pinned_);
@@ -1810,7 +1812,7 @@ void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, c
   // near-field rows (HBM-bound) run on a forked stream, overlapping the
   // latency-bound upward/downward passes and the FP64-bound far field
   S* nrows = reinterpret_cast<S*>(d_nrows_);
-  if (pev == nullptr) {
+  if (pev == nullptr && !near_in_phase2_) {
     IGB_CUDA(cudaEventRecord(ev_fork_, s));
     IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
     k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
@@ -1858,6 +1860,14 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
   auto mark = [&](int i) {
     if (pev) IGB_CUDA(cudaEventRecord(pev[i], s));
   };
+  if (pev == nullptr && near_in_phase2_) {  // graph mode: near rows overlap all of phase 2
+    IGB_CUDA(cudaEventRecord(ev_fork_, s));
+    IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+    k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
+        nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
+    ++launches;
+    IGB_CUDA(cudaEventRecord(ev_join_, side_));
+  }
   if (Lp.world > 1) {
     const long long tot = static_cast<long long>(Lp.world) * Lp.pack_max * rows;
     k_unpack<S><<<grid_for(tot, 256), 256, 0, s>>>(Lp.world * Lp.pack_max, d_unpack_nodes_, rows,
@@ -2097,17 +2107,47 @@ void H2Device::dispatch_kind(F&& f) {
   }
 }
 
+// Multi-GPU matvec phases as two CUDA graphs over the handle's buffers (one
+// graph launch each instead of ~20 kernel launches); the caller's collectives
+// run between them on its stream.  The near rows are forked at the start of
+// phase 2 (coefficients come from phase 1) and joined before the leaf transform.
 void H2Device::dist_phase1(const double* x, double* send, cudaStream_t s) {
   IGB_CUDA(cudaSetDevice(device_));
-  int n = 0;
-  dispatch_kind([&](auto kt) { enqueue_phase1<decltype(kt)>(x, send, s, nullptr, n); });
-  phase1_launches_ = n;
+  const size_t sw = is_complex() ? 16 : 8;
+  if (!graph1_) {
+    cudaGraph_t graph;
+    int n = 0;
+    near_in_phase2_ = true;
+    IGB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    dispatch_kind([&](auto kt) { enqueue_phase1<decltype(kt)>(dx_, d_send_, stream_, nullptr, n); });
+    IGB_CUDA(cudaStreamEndCapture(stream_, &graph));
+    IGB_CUDA(cudaGraphInstantiate(&graph1_, graph, 0));
+    cudaGraphDestroy(graph);
+    phase1_launches_ = n;
+  }
+  IGB_CUDA(cudaMemcpyAsync(dx_, x, static_cast<size_t>(dim()) * sw, cudaMemcpyDeviceToDevice, s));
+  IGB_CUDA(cudaGraphLaunch(graph1_, s));
+  if (send_count() > 0 && send != nullptr)
+    IGB_CUDA(cudaMemcpyAsync(send, d_send_, send_count() * sw, cudaMemcpyDeviceToDevice, s));
 }
 void H2Device::dist_phase2(const double* recv, double* y, cudaStream_t s) {
   IGB_CUDA(cudaSetDevice(device_));
-  int n = 0;
-  dispatch_kind([&](auto kt) { enqueue_phase2<decltype(kt)>(recv, y, s, nullptr, n); });
-  apply_launches_ = phase1_launches_ + n;
+  const size_t sw = is_complex() ? 16 : 8;
+  if (!graph2_) {
+    cudaGraph_t graph;
+    int n = 0;
+    near_in_phase2_ = true;
+    IGB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    dispatch_kind([&](auto kt) { enqueue_phase2<decltype(kt)>(d_recv_, dy_, stream_, nullptr, n); });
+    IGB_CUDA(cudaStreamEndCapture(stream_, &graph));
+    IGB_CUDA(cudaGraphInstantiate(&graph2_, graph, 0));
+    cudaGraphDestroy(graph);
+    apply_launches_ = phase1_launches_ + n;
+  }
+  if (lp_.world > 1 && send_count() > 0)
+    IGB_CUDA(cudaMemcpyAsync(d_recv_, recv, send_count() * lp_.world * sw, cudaMemcpyDeviceToDevice, s));
+  IGB_CUDA(cudaGraphLaunch(graph2_, s));
+  IGB_CUDA(cudaMemcpyAsync(y, dy_, static_cast<size_t>(dim()) * sw, cudaMemcpyDeviceToDevice, s));
 }
 
 void H2Device::enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev) {

@@ -161,6 +161,8 @@ class H2Device {
   cudaStream_t side_ = nullptr, side2_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_fork2_ = nullptr, ev_join2_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
+  cudaGraphExec_t graph1_ = nullptr, graph2_ = nullptr;  // multi-GPU phases
+  bool near_in_phase2_ = false;  // set while capturing the phase graphs
   int apply_launches_ = 0, phase1_launches_ = 0;
   int assembly_kernels_ = 0, assembly_launches_count_ = 0;
   size_t upload_bytes_ = 0;
