@@ -229,6 +229,11 @@ int igb_rhs_assemble(const igb_discretization* d, int quad_order, int device, co
  * Scalar per point, Maxwell 3 complex per point */
 int igb_potential(const igb_discretization* d, const double* density, int n_points, const double* points,
                   int quad_order, int device, double* out);
+/* assemble_dense / assemble_dense_complex (assembly.cpp:16-53, assembly.hpp:25-28):
+ * the dense Galerkin matrix on the device, `out` = host, column-major
+ * dof_count x dof_count Scalar (Eigen MatrixXd / MatrixXcd memory); orders 0 ->
+ * P+2 / P+3 as AssemblyOptions */
+int igb_dense_assemble(const igb_discretization* d, int far_order, int sing_order, int device, double* out);
 
 /* eta-admissibility of two boxes (min xyz, max xyz), h2.cpp:92-97 */
 int igb_admissible(const double box_a[6], const double box_b[6], double eta);

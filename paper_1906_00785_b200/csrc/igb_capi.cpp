@@ -588,6 +588,14 @@ int igb_potential(const igb_discretization* d, const double* density, int n_poin
   });
 }
 
+int igb_dense_assemble(const igb_discretization* d, int far_order, int sing_order, int device, double* out) {
+  return guard([&] {
+    need(d, "discretization");
+    need(out, "out");
+    igb::dense_assemble(*d->d, far_order, sing_order, device, out);
+  });
+}
+
 int igb_admissible(const double a[6], const double b[6], double eta) {
   igb::Box A, B;
   for (int k = 0; k < 3; ++k) {

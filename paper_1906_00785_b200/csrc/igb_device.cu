@@ -171,37 +171,21 @@ __global__ void __launch_bounds__(256) k_couplings(long long n_pairs, int mm, co
 
 // --------------------------------------------------- K4: regular near
 // blk = sum_c w_c A_c^T (K B_c)  (pair_integration.hpp:76-95)
-// Regular near blocks (pair_integration.hpp far_block 76-95): tensor Gauss on
-// both elements from the element caches.  One CTA integrates P unique pairs
-// (ea < eb); the block goes to the slot of (ea, eb) and its transpose to the
-// slot of (eb, ea) (either may be another rank's, -1).
-template <class KT>
-__global__ void __launch_bounds__(128) k_regular(int n_pairs, int P, const int* __restrict__ slot_ab,
-                                                 const int* __restrict__ slot_ba, const int* __restrict__ near_a,
-                                                 const int* __restrict__ near_b, const int* __restrict__ near_rs,
-                                                 const int* __restrict__ near_ea, int nq,
-                                                 const double* __restrict__ cpts, const double* __restrict__ cval,
-                                                 KParams kp, double* __restrict__ near) {
+// Regular blocks (pair_integration.hpp far_block 76-95): tensor Gauss on both
+// elements from the element caches, np pairs per CTA (one work item per
+// thread).  pair(p, ea, eb) names pair p; put(p, la, lb, v) stores entry
+// (la, lb) of its block.
+template <class KT, class PairFn, class PutFn>
+__device__ __forceinline__ void regular_body(int np, int nq, const double* __restrict__ cpts,
+                                             const double* __restrict__ cval, KParams kp, PairFn pair, PutFn put) {
   using S = typename KT::S;
   constexpr int NL = KT::NL, NC = KT::NC;
   extern __shared__ __align__(16) double sm[];
-  S* KB = reinterpret_cast<S*>(sm);  // [P][NC][nq][NL]
-  const int p0 = blockIdx.x * P, np = min(P, n_pairs - p0);
-  auto elems = [&](int p, int& ea, int& eb) {
-    const int qab = slot_ab[p0 + p];
-    if (qab >= 0) {
-      ea = near_ea[qab];
-      eb = near_b[qab];
-    } else {
-      const int qba = slot_ba[p0 + p];
-      ea = near_b[qba];
-      eb = near_ea[qba];
-    }
-  };
+  S* KB = reinterpret_cast<S*>(sm);  // [np][NC][nq][NL]
   for (int it = threadIdx.x; it < np * NC * nq; it += blockDim.x) {
     const int p = it / (NC * nq), r = it % (NC * nq), c = r / nq, i = r % nq;
     int ea, eb;
-    elems(p, ea, eb);
+    pair(p, ea, eb);
     const double* pa = cpts + static_cast<size_t>(ea) * nq * 3;
     const double* pb = cpts + static_cast<size_t>(eb) * nq * 3;
     const double xa = pa[3 * i], ya = pa[3 * i + 1], za = pa[3 * i + 2];
@@ -219,11 +203,10 @@ __global__ void __launch_bounds__(128) k_regular(int n_pairs, int P, const int* 
     for (int l = 0; l < NL; ++l) KB[((p * NC + c) * nq + i) * NL + l] = acc[l];
   }
   __syncthreads();
-  S* out = reinterpret_cast<S*>(near);
   for (int o = threadIdx.x; o < np * NL * NL; o += blockDim.x) {
     const int p = o / (NL * NL), la = (o / NL) % NL, lb = o % NL;
     int ea, eb;
-    elems(p, ea, eb);
+    pair(p, ea, eb);
     S tot = zero<S>();
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -235,10 +218,111 @@ __global__ void __launch_bounds__(128) k_regular(int n_pairs, int P, const int* 
       }
       tot = tot + s;
     }
-    const int qab = slot_ab[p0 + p], qba = slot_ba[p0 + p];
-    if (qab >= 0) out[near_off(near_a, near_rs, qab, la, lb, NL)] = tot;
-    if (qba >= 0) out[near_off(near_a, near_rs, qba, lb, la, NL)] = tot;
+    put(p, la, lb, tot);
   }
+}
+
+// Regular near blocks of the H2 near field: P unique pairs (ea < eb) per CTA;
+// the block goes to the slot of (ea, eb) and its transpose to the slot of
+// (eb, ea) (either may be another rank's, -1).
+template <class KT>
+__global__ void __launch_bounds__(128) k_regular(int n_pairs, int P, const int* __restrict__ slot_ab,
+                                                 const int* __restrict__ slot_ba, const int* __restrict__ near_a,
+                                                 const int* __restrict__ near_b, const int* __restrict__ near_rs,
+                                                 const int* __restrict__ near_ea, int nq,
+                                                 const double* __restrict__ cpts, const double* __restrict__ cval,
+                                                 KParams kp, double* __restrict__ near) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL;
+  const int p0 = blockIdx.x * P, np = min(P, n_pairs - p0);
+  S* out = reinterpret_cast<S*>(near);
+  regular_body<KT>(
+      np, nq, cpts, cval, kp,
+      [&](int p, int& ea, int& eb) {
+        const int qab = slot_ab[p0 + p];
+        if (qab >= 0) {
+          ea = near_ea[qab];
+          eb = near_b[qab];
+        } else {
+          const int qba = slot_ba[p0 + p];
+          ea = near_b[qba];
+          eb = near_ea[qba];
+        }
+      },
+      [&](int p, int la, int lb, S v) {
+        const int qab = slot_ab[p0 + p], qba = slot_ba[p0 + p];
+        if (qab >= 0) out[near_off(near_a, near_rs, qab, la, lb, NL)] = v;
+        if (qba >= 0) out[near_off(near_a, near_rs, qba, lb, la, NL)] = v;
+      });
+}
+
+// ---- dense Galerkin matrix (assembly.cpp:16-53)
+// all pairs (ea, eb), ea in [ea0, ea0 + nrow): regular blocks into the chunk
+// buffer buf[(ea - ea0) * ne + eb][la][lb] (singular pairs overwritten next)
+template <class KT>
+__global__ void __launch_bounds__(128) k_regular_dense(long long n_pairs, int P, int ea0, int ne, int nq,
+                                                       const double* __restrict__ cpts,
+                                                       const double* __restrict__ cval, KParams kp,
+                                                       double* __restrict__ buf) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL;
+  const long long p0 = static_cast<long long>(blockIdx.x) * P;
+  const int np = static_cast<int>(min(static_cast<long long>(P), n_pairs - p0));
+  S* out = reinterpret_cast<S*>(buf);
+  regular_body<KT>(
+      np, nq, cpts, cval, kp,
+      [&](int p, int& ea, int& eb) {
+        const long long g = p0 + p;
+        ea = ea0 + static_cast<int>(g / ne);
+        eb = static_cast<int>(g % ne);
+      },
+      [&](int p, int la, int lb, S v) { out[((p0 + p) * NL + la) * NL + lb] = v; });
+}
+// singular blocks (compact, ea <= eb) of the pairs with a row in the chunk;
+// ea > eb rows get the transpose (pair_integration.hpp:139-148)
+template <class S, int NL>
+__global__ void k_dense_sing_place(int n_items, const int* __restrict__ ea, const int* __restrict__ eb,
+                                   const S* __restrict__ blk, int ea0, int nrow, int ne, S* __restrict__ buf) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n_items) * NL * NL) return;
+  const int k = static_cast<int>(idx / (NL * NL)), o = static_cast<int>(idx % (NL * NL)), la = o / NL, lb = o % NL;
+  const int a = ea[k], b = eb[k];
+  const S v = blk[idx];
+  if (a >= ea0 && a < ea0 + nrow) buf[((static_cast<size_t>(a - ea0) * ne + b) * NL + la) * NL + lb] = v;
+  if (a != b && b >= ea0 && b < ea0 + nrow) buf[((static_cast<size_t>(b - ea0) * ne + a) * NL + lb) * NL + la] = v;
+}
+// row strips: strip[(ea - ea0) nl + la][j] = sum over the incidences (eb, lb)
+// of DOF j in ascending (eb, lb) of sign * block(ea, eb)[la][lb]
+template <class S, int NL>
+__global__ void k_dense_strip(int nrow, int nd, int ne, const int* __restrict__ dof_start,
+                              const int* __restrict__ dof_inc, const double* __restrict__ sg,
+                              const S* __restrict__ buf, S* __restrict__ strip) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(nrow) * NL * nd) return;
+  const int j = static_cast<int>(idx % nd), r = static_cast<int>(idx / nd), el = r / NL, la = r % NL;
+  S acc = zero<S>();
+  for (int i = dof_start[j]; i < dof_start[j + 1]; ++i) {
+    const int k = dof_inc[i], eb = k / NL, lb = k % NL;
+    acc = acc + buf[((static_cast<size_t>(el) * ne + eb) * NL + la) * NL + lb] * sg[k];
+  }
+  strip[idx] = acc;
+}
+// a(i, j) += sign * strip row of every incidence (ea, la) of DOF i inside the
+// chunk, ascending ea (column-major a; the reference's fixed-order reduction)
+template <class S, int NL>
+__global__ void k_dense_rows(int n_rows, const int* __restrict__ rows, int nd, const int* __restrict__ dof_start,
+                             const int* __restrict__ dof_inc, const double* __restrict__ sg, int ea0, int nrow,
+                             const S* __restrict__ strip, S* __restrict__ A) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n_rows) * nd) return;
+  const int j = static_cast<int>(idx % nd), i = rows[idx / nd];
+  S acc = A[static_cast<size_t>(j) * nd + i];
+  for (int q = dof_start[i]; q < dof_start[i + 1]; ++q) {
+    const int k = dof_inc[q], ea = k / NL;
+    if (ea < ea0 || ea >= ea0 + nrow) continue;
+    acc = acc + strip[static_cast<size_t>((ea - ea0) * NL + k % NL) * nd + j] * sg[k];
+  }
+  A[static_cast<size_t>(j) * nd + i] = acc;
 }
 
 // ---------------------------------------------------- K5: singular near
@@ -2330,6 +2414,213 @@ void H2Device::images(double* out) const {
   IGB_CUDA(cudaSetDevice(device_));
   IGB_CUDA(cudaMemcpy(out, d_img_, static_cast<size_t>(plan_.n_nodes) * plan_.m * plan_.m * 3 * 8,
                       cudaMemcpyDeviceToHost));
+}
+
+// ====================================================== dense assembly
+// Dense Galerkin matrix (assembly.cpp:16-53) on one device, column-major
+// nd x nd Scalar in `out` (host).  Test elements are processed in chunks that
+// fit a ~1 GB block buffer: all (ea, eb) blocks of the chunk (regular tensor
+// Gauss, then the singular items from the mesh topology), the row strips
+// gathered per trial DOF, and the strips added to the DOF rows in ascending
+// test element -- the reference's summation structure.
+template <class KT>
+static void dense_impl(const Discretization& d, int far_order, int sing_order, int device, double* out) {
+  using S = typename KT::S;
+  constexpr int NL = KT::NL, NC = KT::NC;
+  const int sw = sizeof(S) / 8;
+  if (d.local_count() != NL) throw std::logic_error("B200 dense: local count mismatch");
+  int nf = 0, ns = 0;
+  check_h2_options(d, 2, 1.0, far_order, sing_order, &nf, &ns);
+  if (ns > 16) throw std::invalid_argument("B200 dense: singular order > 16 not supported");
+  int ndev = 0;
+  IGB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) throw std::invalid_argument("assemble_dense: CUDA device index out of range");
+  IGB_CUDA(cudaSetDevice(device));
+  const int ne = d.element_count(), nd = d.dof_count(), nq = nf * nf, m = 2;
+  std::vector<void*> mem;
+  cudaStream_t st = nullptr;
+  auto alloc = [&](size_t bytes) {
+    void* p = nullptr;
+    IGB_CUDA(cudaMalloc(&p, bytes ? bytes : 8));
+    mem.push_back(p);
+    return p;
+  };
+  auto up = [&](const auto& v) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    T* p = static_cast<T*>(alloc(v.size() * sizeof(T)));
+    if (!v.empty()) IGB_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  };
+  try {
+    IGB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<double> cells(d.cells().size() * kCellStride, 0.0);
+    for (size_t c = 0; c < d.cells().size(); ++c) {
+      const GeomCell& gc = d.cells()[c];
+      for (int comp = 0; comp < 4; ++comp)
+        for (int j = 0; j <= kMaxGeomDeg; ++j)
+          for (int i = 0; i <= kMaxGeomDeg; ++i) cells[c * kCellStride + comp * 25 + j * 5 + i] = gc.coef[comp][j][i];
+      cells[c * kCellStride + 100] = gc.u0;
+      cells[c * kCellStride + 101] = gc.v0;
+    }
+    const double* d_cells = up(cells);
+    const int* d_el_cell = up(d.element_cell());
+    const double* d_tab_a = up(d.is_vector() ? d.tab_p() : d.tab_s());
+    const double* d_tab_b = up(d.is_vector() ? d.tab_q() : std::vector<double>(1, 0.0));
+    const double* d_lsign = up(d.lsign());
+    std::vector<double> gxf, gwf, gxs, gws;
+    gauss_rule(nf, gxf, gwf);
+    gauss_rule(ns, gxs, gws);
+    const double *d_gxf = up(gxf), *d_gwf = up(gwf), *d_gxs = up(gxs), *d_gws = up(gws);
+    const std::vector<double> cheb = cheb_nodes(m);
+    std::vector<double> lag(static_cast<size_t>(m) * nf), tmp(m);
+    for (int a = 0; a < nf; ++a) {
+      lagrange_all(cheb, gxf[a], tmp.data());
+      for (int i = 0; i < m; ++i) lag[i * nf + a] = tmp[i];
+    }
+    const double* d_lag = up(lag);
+    double kp4[4] = {d.kappa().real(), d.kappa().imag(), 0.0, 0.0};
+    if (d.is_vector()) {
+      const cplx dw = -1.0 / (d.kappa() * d.kappa());
+      kp4[2] = dw.real();
+      kp4[3] = dw.imag();
+    }
+    const GeoArgs g = geo_args(d, d_cells, d_el_cell, d_tab_a, d_tab_b, kp4);
+    // element caches (+ moments of a 2-point interpolation, unused)
+    double* d_cpts = static_cast<double*>(alloc(static_cast<size_t>(ne) * nq * 3 * 8));
+    double* d_cval = static_cast<double*>(alloc(static_cast<size_t>(ne) * NC * nq * NL * 8));
+    double* d_mom = static_cast<double*>(alloc(static_cast<size_t>(ne) * NL * (d.is_vector() ? 4 : 1) * m * m * 8));
+    {
+      const size_t smem = (104 + KT::TABN + static_cast<size_t>(nq) * NC * NL) * 8;
+      IGB_CUDA(cudaFuncSetAttribute(k_element<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      if (ne > 0) k_element<KT><<<ne, 128, smem, st>>>(g, nf, d_gxf, d_gwf, m, d_lag, d_cpts, d_cval, d_mom);
+      IGB_CUDA(cudaGetLastError());
+    }
+    // singular items (ea <= eb) from the mesh topology, compact blocks
+    SingList items[4];
+    d.singular_items(nullptr, items);
+    const int *d_ia[4] = {}, *d_ib[4] = {};
+    S* d_sblk[4] = {};
+    {
+      using LY = SingLayout<KT>;
+      auto launch = [&](auto cls_tag) {
+        constexpr int CLS = decltype(cls_tag)::value;
+        const SingList& L = items[CLS];
+        d_ia[CLS] = up(L.ea);
+        d_ib[CLS] = up(L.eb);
+        d_sblk[CLS] = static_cast<S*>(alloc(L.ea.size() * NL * NL * sizeof(S)));
+        if (L.ea.empty()) return;
+        SingArgs A;
+        A.n_pairs = static_cast<int>(L.ea.size());
+        A.n = ns;
+        A.ea = d_ia[CLS];
+        A.eb = d_ib[CLS];
+        A.map_a = up(L.map_a);
+        A.map_b = up(L.map_b);
+        A.gx = d_gxs;
+        A.gw = d_gws;
+        A.out = reinterpret_cast<double*>(d_sblk[CLS]);
+        IGB_CUDA(cudaFuncSetAttribute(k_singular<KT, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(LY::BYTES)));
+        k_singular<KT, CLS><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
+        IGB_CUDA(cudaGetLastError());
+      };
+      launch(std::integral_constant<int, 3>{});
+      launch(std::integral_constant<int, 2>{});
+      launch(std::integral_constant<int, 1>{});
+    }
+    // DOF incidence, ascending (e, l)
+    std::vector<int> dstart(nd + 1, 0), dinc(d.l2g().size());
+    for (int k : d.l2g()) ++dstart[k + 1];
+    for (int i = 0; i < nd; ++i) dstart[i + 1] += dstart[i];
+    {
+      std::vector<int> fill(dstart.begin(), dstart.end() - 1);
+      for (size_t k = 0; k < d.l2g().size(); ++k) dinc[fill[d.l2g()[k]]++] = static_cast<int>(k);
+    }
+    const int *d_dstart = up(dstart), *d_dinc = up(dinc);
+    // chunk of test elements: block buffer and strips within ~1 GB each
+    const size_t row_blk = static_cast<size_t>(ne) * NL * NL * sizeof(S), row_strip = static_cast<size_t>(NL) * nd * sizeof(S);
+    const size_t budget = size_t(1) << 30;
+    const int nrow = static_cast<int>(std::max<size_t>(1, std::min<size_t>(ne, budget / std::max(row_blk, row_strip))));
+    S* d_buf = static_cast<S*>(alloc(static_cast<size_t>(nrow) * row_blk));
+    S* d_strip = static_cast<S*>(alloc(static_cast<size_t>(nrow) * row_strip));
+    S* d_A = static_cast<S*>(alloc(static_cast<size_t>(nd) * nd * sizeof(S)));
+    int* d_rows = static_cast<int*>(alloc(static_cast<size_t>(nd) * sizeof(int)));
+    IGB_CUDA(cudaMemsetAsync(d_A, 0, static_cast<size_t>(nd) * nd * sizeof(S), st));
+    const int per = std::max(1, 128 / (NC * nq));
+    const size_t rsmem = static_cast<size_t>(per) * NC * nq * NL * sizeof(S);
+    IGB_CUDA(cudaFuncSetAttribute(k_regular_dense<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (rsmem > 200 * 1024) throw std::invalid_argument("B200 dense: far quadrature order too large");
+    KParams kp;
+    kp.kr = kp4[0];
+    kp.ki = kp4[1];
+    kp.dwx = kp4[2];
+    kp.dwy = kp4[3];
+    for (int ea0 = 0; ea0 < ne; ea0 += nrow) {
+      const int nr = std::min(nrow, ne - ea0);
+      const long long npair = static_cast<long long>(nr) * ne;
+      k_regular_dense<KT><<<static_cast<unsigned>((npair + per - 1) / per), 128, rsmem, st>>>(
+          npair, per, ea0, ne, nq, d_cpts, d_cval, kp, reinterpret_cast<double*>(d_buf));
+      for (int c = 1; c <= 3; ++c) {
+        const long long tot = static_cast<long long>(items[c].ea.size()) * NL * NL;
+        if (tot)
+          k_dense_sing_place<S, NL><<<grid_for(tot, 256), 256, 0, st>>>(static_cast<int>(items[c].ea.size()), d_ia[c],
+                                                                        d_ib[c], d_sblk[c], ea0, nr, ne, d_buf);
+      }
+      const long long ns_ = static_cast<long long>(nr) * NL * nd;
+      k_dense_strip<S, NL><<<grid_for(ns_, 256), 256, 0, st>>>(nr, nd, ne, d_dstart, d_dinc, d_lsign, d_buf, d_strip);
+      std::vector<int> rows;
+      for (int e = ea0; e < ea0 + nr; ++e)
+        for (int l = 0; l < NL; ++l) rows.push_back(d.l2g()[static_cast<size_t>(e) * NL + l]);
+      std::sort(rows.begin(), rows.end());
+      rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+      IGB_CUDA(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      const long long nrw = static_cast<long long>(rows.size()) * nd;
+      k_dense_rows<S, NL><<<grid_for(nrw, 256), 256, 0, st>>>(static_cast<int>(rows.size()), d_rows, nd, d_dstart,
+                                                              d_dinc, d_lsign, ea0, nr, d_strip, d_A);
+      IGB_CUDA(cudaGetLastError());
+      IGB_CUDA(cudaStreamSynchronize(st));  // the host row list is reused next chunk
+    }
+    IGB_CUDA(cudaMemcpyAsync(out, d_A, static_cast<size_t>(nd) * nd * sizeof(S), cudaMemcpyDeviceToHost, st));
+    IGB_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : mem) cudaFree(p);
+    if (st) cudaStreamDestroy(st);
+    throw;
+  }
+  for (void* p : mem) cudaFree(p);
+  cudaStreamDestroy(st);
+}
+
+void dense_assemble(const Discretization& d, int far_order, int sing_order, int device, double* out) {
+  const int kind = d.kind();
+  const int q = kind == kMaxwell ? d.degree() : d.scalar_degree();
+  if (kind == kMaxwell && (q < 1 || q > 3)) throw std::invalid_argument("B200 dense: Maxwell degree > 3 not instantiated");
+  if (kind != kMaxwell && (q < 0 || q > 4)) throw std::invalid_argument("B200 dense: scalar degree > 4 not instantiated");
+  auto run = [&](auto kt) { dense_impl<decltype(kt)>(d, far_order, sing_order, device, out); };
+  if (kind == kLaplace) {
+    switch (q) {
+      case 0: run(LapT<0>{}); break;
+      case 1: run(LapT<1>{}); break;
+      case 2: run(LapT<2>{}); break;
+      case 3: run(LapT<3>{}); break;
+      default: run(LapT<4>{}); break;
+    }
+  } else if (kind == kHelmholtz) {
+    switch (q) {
+      case 0: run(HelmT<0>{}); break;
+      case 1: run(HelmT<1>{}); break;
+      case 2: run(HelmT<2>{}); break;
+      case 3: run(HelmT<3>{}); break;
+      default: run(HelmT<4>{}); break;
+    }
+  } else {
+    switch (q) {
+      case 1: run(MaxT<1>{}); break;
+      case 2: run(MaxT<2>{}); break;
+      default: run(MaxT<3>{}); break;
+    }
+  }
 }
 
 }  // namespace igb

@@ -176,4 +176,8 @@ class H2Device {
   } as_;
 };
 
+// Dense Galerkin matrix (assembly.cpp:16-53) on one device; `out`: host,
+// column-major dof_count^2 Scalar (interleaved complex for Helmholtz/Maxwell)
+void dense_assemble(const Discretization& d, int far_order, int sing_order, int device, double* out);
+
 }  // namespace igb

@@ -86,7 +86,7 @@ SYMBOLS = (
     "igb_h2_dim", "igb_h2_apply", "igb_h2_apply_device", "igb_h2_storage_report", "igb_h2_counts",
     "igb_h2_near_pairs", "igb_h2_far_pairs", "igb_h2_tree", "igb_h2_near_blocks", "igb_h2_couplings",
     "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
-    "igb_h2_gmres", "igb_h2_cg", "igb_rhs_points", "igb_rhs_assemble", "igb_potential",
+    "igb_h2_gmres", "igb_h2_cg", "igb_rhs_points", "igb_rhs_assemble", "igb_potential", "igb_dense_assemble",
     "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_counts", "igb_plan_near_pairs",
     "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
@@ -165,6 +165,7 @@ def lib():
     L.igb_rhs_points.argtypes = [vp, i32, i32, P(f64), P(i32)]
     L.igb_rhs_assemble.argtypes = [vp, i32, i32, P(f64), P(f64)]
     L.igb_potential.argtypes = [vp, P(f64), i32, P(f64), i32, i32, P(f64)]
+    L.igb_dense_assemble.argtypes = [vp, i32, i32, i32, P(f64)]
     L.igb_admissible.argtypes = [P(f64), P(f64), f64]
     L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
     _LIB = L
@@ -711,6 +712,17 @@ def eval_potential(disc: Discretization, density, points, quad_order=10, device=
 
 
 eval_maxwell_potential = eval_potential
+
+
+def assemble_dense(disc: Discretization, opts: AssemblyOptions | None = None, device: int = 0):
+    """assemble_dense / assemble_dense_complex (assembly.cpp:16-53) on the B200:
+    the dense Galerkin matrix (dof_count x dof_count, float64 or complex128)."""
+    opts = opts or AssemblyOptions()
+    n = disc.dof_count()
+    dt = np.complex128 if disc.pde().is_complex() else np.float64
+    a = np.zeros((n, n), dtype=dt, order="F")
+    _check(lib().igb_dense_assemble(disc._h, int(opts.far_order), int(opts.sing_order), int(device), _p(a)))
+    return a
 
 
 def make_sphere_grid(radius, n, center=(0.0, 0.0, 0.0)):
