@@ -1123,8 +1123,9 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
 
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
 // in ascending t (fixed order)
-// (single GPU: every pair slot was written -- unconditional, unrolled stream
-// over the row's contiguous slots; multi-GPU: only pairs with an owned source)
+// Unconditional, unrolled stream over the row's contiguous slots.  Multi-GPU:
+// only owned rows; the slots of pairs whose other node is another rank's are
+// never written and stay zero from construction.
 // rows: 0 all, 1 leaf-level rows only, 2 the other levels (level-split graph)
 template <bool DIST>
 __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs, const int* __restrict__ upper_start,
@@ -1139,13 +1140,9 @@ __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs,
   if (q0 == q1 || (DIST && !owned[s])) return;
   double acc = down[idx];
   const double* sp = slot + static_cast<size_t>(q0) * mm + nu;
-  if constexpr (DIST) {
-    for (int q = q0; q < q1; ++q, sp += mm)
-      if (owned[far_b[q]]) acc += *sp;
-  } else {
+  (void)far_b;
 #pragma unroll 8
-    for (int q = q0; q < q1; ++q, sp += mm) acc += __ldcs(sp);  // read once: streaming
-  }
+  for (int q = q0; q < q1; ++q, sp += mm) acc += __ldcs(sp);  // read once: streaming
   down[idx] = acc;
 }
 
@@ -1690,6 +1687,9 @@ void H2Device::stage_plan() {
       d_upper_start_ = upload(P.far_upper_start);
       d_trans_ = upload(P.far_trans);
       d_slot_ = dalloc<double>(P.far_a.size() * static_cast<size_t>(mm));
+      // slots no kernel writes (multi-GPU: pairs with another rank's node) read as 0
+      IGB_CUDA(cudaMemsetAsync(d_slot_, 0, P.far_a.size() * static_cast<size_t>(mm) * sizeof(double),
+                               up_stream_ ? up_stream_ : stream_));
     }
   }
   d_dof_start_ = upload(Lp.dof_start);
@@ -1917,7 +1917,7 @@ void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, c
   if (Lp.world > 1 && Lp.pack_nodes.size()) {
     const long long tot = static_cast<long long>(Lp.pack_nodes.size()) * rows;
     k_pack<S><<<grid_for(tot, 256), 256, 0, s>>>(static_cast<int>(Lp.pack_nodes.size()), d_pack_nodes_, rows, up,
-                                                  reinterpret_cast<S*>(send));
+                                                  reinterpret_cast<S*>(send ? send : d_send_));
     ++launches;
   }
 }
@@ -1955,7 +1955,7 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
   if (Lp.world > 1) {
     const long long tot = static_cast<long long>(Lp.world) * Lp.pack_max * rows;
     k_unpack<S><<<grid_for(tot, 256), 256, 0, s>>>(Lp.world * Lp.pack_max, d_unpack_nodes_, rows,
-                                                    reinterpret_cast<const S*>(recv), up);
+                                                    reinterpret_cast<const S*>(recv ? recv : d_recv_), up);
     ++launches;
   }
   if (L >= 1) {  // roots (replicated on every rank)
@@ -2263,6 +2263,10 @@ void H2Device::enqueue_apply_dispatch(const double* x, double* y, cudaStream_t s
 }
 
 void H2Device::launch_apply_graph(cudaStream_t s) {
+  if (lp_.world > 1)
+    throw std::logic_error(
+        "H2Matrix: a rank of a distributed operator is applied with dist_phase1 / all-gather / dist_phase2 / "
+        "all-reduce (DistH2Matrix)");
   IGB_CUDA(cudaSetDevice(device_));
   if (!graph_exec_) {
     cudaGraph_t graph;

@@ -56,3 +56,15 @@ def test_row_partition_matvec(igb, case, world):
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) < 1e-13
     # the block rows are split, not replicated
     assert sum(h.device_bytes()["near"] for h in hs) == full.device_bytes()["near"]
+
+
+def test_rank_handle_rejects_single_apply(igb):
+    # a rank of a distributed operator holds only its block rows: the
+    # single-operator apply must refuse (LogicError), not read unset buffers
+    import numpy as np
+    d = igb.Discretization(igb.make_sphere(), igb.Pde.laplace(), 1, 1, 2)
+    h = igb.H2Matrix(d, igb.H2Options(m=4), world=2, rank=1)
+    with pytest.raises(igb.LogicError):
+        h @ np.ones(d.dof_count())
+    p = h.profile_apply(2)  # per-rank phase timing stays available (own buffers)
+    assert all(v >= 0 for v in p.values())
