@@ -1676,6 +1676,11 @@ void H2Device::stage_plan() {
       std::vector<int> sym_targets;
       for (int t : Lp.far_targets)
         if (Lp.world > 1 || P.far_upper_start[t] < P.far_row_start[t + 1]) sym_targets.push_back(t);
+      // longest rows first (one warp per target): the last wave holds the light rows
+      auto work = [&](int t) {
+        return Lp.world > 1 ? P.far_row_start[t + 1] - P.far_row_start[t] : P.far_row_start[t + 1] - P.far_upper_start[t];
+      };
+      std::stable_sort(sym_targets.begin(), sym_targets.end(), [&](int a, int b) { return work(a) > work(b); });
       n_sym_targets_ = static_cast<int>(sym_targets.size());
       d_sym_targets_ = upload(sym_targets);
       std::vector<int> fine, coarse;
