@@ -34,6 +34,12 @@ __host__ __device__ __forceinline__ cd mk(double a, double b) {
   return r;
 }
 template <class S>
+__host__ __device__ __forceinline__ S mk_s(double re, double im);
+template <>
+__host__ __device__ __forceinline__ double mk_s<double>(double re, double) { return re; }
+template <>
+__host__ __device__ __forceinline__ cd mk_s<cd>(double re, double im) { return mk(re, im); }
+template <class S>
 __device__ __forceinline__ S zero();
 template <>
 __device__ __forceinline__ double zero<double>() { return 0.0; }
@@ -65,6 +71,10 @@ __device__ __forceinline__ cd shfl_down(cd v, int o) {
 __device__ __forceinline__ double shfl_idx(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ cd shfl_idx(cd v, int src) {
   return mk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ double shfl_xor(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ cd shfl_xor(cd v, int o) {
+  return mk(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
 }
 __device__ __forceinline__ double ldg_s(const double* p) { return __ldg(p); }
 __device__ __forceinline__ cd ldg_s(const cd* p) {

@@ -983,6 +983,118 @@ __global__ void __launch_bounds__(256) k_far_fused(int n_targets, const int* __r
   }
 }
 
+// Symmetric fused far field, warp-row layout (complex kinds, Maxwell channels,
+// m >= 6): K(s,t) = K(t,s)^T, so each unordered admissible pair {t, s}, t < s,
+// is evaluated once by the warp of t.  Lane owns target rows nu = lane + 32 r;
+// the source cluster's points and moments are staged in shared memory; per
+// source point mu each lane accumulates K up[s] into its rows and its share of
+// (K^T up[t])[mu], which a fixed xor tree sums over the warp.  The products
+// (channel weight w_c applied, Maxwell: -1/kappa^2 on the divergence channel)
+// go to the slot of the transposed pair, summed by k_far_lower.
+template <class KT, int R>
+__global__ void __launch_bounds__(256) k_far_sym_w(int n_targets, const int* __restrict__ targets,
+                                                   const int* __restrict__ upper_start,
+                                                   const int* __restrict__ far_rs, const int* __restrict__ far_b,
+                                                   const int* __restrict__ trans, const double* __restrict__ img,
+                                                   int mm, const typename KT::S* __restrict__ up, KParams kp,
+                                                   typename KT::S* __restrict__ down,
+                                                   typename KT::S* __restrict__ slot) {
+  using S = typename KT::S;
+  constexpr int NCH = KT::NC;
+  constexpr int SW = sizeof(S) / 8;
+  constexpr int PW = ((4 + NCH * SW) + 1) / 2 * 2;
+  extern __shared__ __align__(16) double smf[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double* gsm = smf + static_cast<size_t>(wib) * 32 * R * PW;
+  if (warp >= n_targets) return;
+  const int t = targets[warp];
+  const int rows = NCH * mm;
+  S wc[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) wc[c] = (NCH == 4 && c == 3) ? mk_s<S>(kp.dwx, kp.dwy) : mk_s<S>(1.0, 0.0);
+  double tx[R][3];
+  S xt[R][NCH], acc[NCH][R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int nu = lane + 32 * r;
+    const bool ok = nu < mm;
+    const double* p = img + (static_cast<size_t>(t) * mm + (ok ? nu : 0)) * 3;
+    tx[r][0] = p[0];
+    tx[r][1] = p[1];
+    tx[r][2] = p[2];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      xt[r][c] = ok ? up[static_cast<size_t>(t) * rows + c * mm + nu] : zero<S>();
+      acc[c][r] = zero<S>();
+    }
+  }
+  for (int q = upper_start[t]; q < far_rs[t + 1]; ++q) {
+    const int s = far_b[q];
+    const double* is = img + static_cast<size_t>(s) * mm * 3;
+    const S* us = up + static_cast<size_t>(s) * rows;
+    for (int mu = lane; mu < mm; mu += 32) {
+      double* d = gsm + mu * PW;
+      d[0] = is[3 * mu];
+      d[1] = is[3 * mu + 1];
+      d[2] = is[3 * mu + 2];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) reinterpret_cast<S*>(d + 4)[c] = us[c * mm + mu];
+    }
+    __syncwarp();
+    S pst[NCH][R];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+      for (int r = 0; r < R; ++r) pst[c][r] = zero<S>();
+    for (int mu = 0; mu < mm; ++mu) {
+      const double* d = gsm + mu * PW;
+      const double2 xy = *reinterpret_cast<const double2*>(d);
+      const double sz = d[2];
+      S xs[NCH], v[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        xs[c] = reinterpret_cast<const S*>(d + 4)[c];
+        v[c] = zero<S>();
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (lane + 32 * r >= mm) continue;
+        const double d0 = tx[r][0] - xy.x, d1 = tx[r][1] - xy.y, d2 = tx[r][2] - sz;
+        const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          fmac(acc[c][r], gk, xs[c]);
+          fmac(v[c], gk, xt[r][c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        S w = v[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w = w + shfl_xor(w, o);
+        if ((mu & 31) == lane) pst[c][mu >> 5] = w;
+      }
+    }
+    S* dst = slot + static_cast<size_t>(trans[q]) * rows;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int mu = lane + 32 * r;
+      if (mu < mm)
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) dst[c * mm + mu] = pst[c][r] * wc[c];
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int nu = lane + 32 * r;
+    if (nu < mm)
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) down[static_cast<size_t>(t) * rows + c * mm + nu] = acc[c][r] * wc[c];
+  }
+}
+
 // Branch-free FP64 reciprocal square root for normal positive inputs:
 // MUFU.RSQ64H seed (rsqrt.approx.ftz.f64, rel. err < 2^-22) + 2 Newton steps.
 __device__ __forceinline__ double rsqrt_nr(double x) {
@@ -1547,6 +1659,10 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_sym_w<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_sym_w<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_sym_w<KT, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_sym_w<KT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaStreamSynchronize(stream_));
   if (verbose) fprintf(stderr, "[igb ctor] scratch cudaMalloc total %.2f ms\n", alloc_ms_);
   lap("scratch");
@@ -1672,7 +1788,9 @@ void H2Device::stage_plan() {
     d_far_targets_ = upload(targets);
     // symmetric fused far field (Laplace, m <= 6): upper pairs + transposes
     sym_far_ = !stored_couplings() && d.kind() == kLaplace && m >= 2 && m <= 6;
-    if (sym_far_) {
+    // other kinds / larger m, one GPU: the warp-row symmetric kernel
+    sym_w_ = !stored_couplings() && !sym_far_ && Lp.world == 1 && mm >= 32 && mm <= 128;
+    if (sym_far_ || sym_w_) {
       std::vector<int> sym_targets;
       for (int t : Lp.far_targets)
         if (Lp.world > 1 || P.far_upper_start[t] < P.far_row_start[t + 1]) sym_targets.push_back(t);
@@ -1691,10 +1809,10 @@ void H2Device::stage_plan() {
       d_sym_coarse_ = upload(coarse);
       d_upper_start_ = upload(P.far_upper_start);
       d_trans_ = upload(P.far_trans);
-      d_slot_ = dalloc<double>(P.far_a.size() * static_cast<size_t>(mm));
+      const size_t per_pair = static_cast<size_t>(mm) * (sym_w_ ? static_cast<size_t>(nch_) * sw : 1);
+      d_slot_ = dalloc<double>(P.far_a.size() * per_pair);
       // slots no kernel writes (multi-GPU: pairs with another rank's node) read as 0
-      IGB_CUDA(cudaMemsetAsync(d_slot_, 0, P.far_a.size() * static_cast<size_t>(mm) * sizeof(double),
-                               up_stream_ ? up_stream_ : stream_));
+      IGB_CUDA(cudaMemsetAsync(d_slot_, 0, P.far_a.size() * per_pair * sizeof(double), up_stream_ ? up_stream_ : stream_));
     }
   }
   d_dof_start_ = upload(Lp.dof_start);
@@ -2022,6 +2140,33 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
       else
         k_far_lower<false><<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(
             P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn);
+    } else if (sym_w_) {
+      KParams kp;
+      kp.kr = as_.kp[0];
+      kp.ki = as_.kp[1];
+      kp.dwx = as_.kp[2];
+      kp.dwy = as_.kp[3];
+      constexpr int PW = ((4 + KT::NC * static_cast<int>(sizeof(S) / 8)) + 1) / 2 * 2;
+      const unsigned gsym = grid_for(static_cast<long long>(n_sym_targets_) * 32, 256);
+      S* sl = reinterpret_cast<S*>(d_slot_);
+      const int R = (mm + 31) / 32;
+      const size_t smem = static_cast<size_t>(8) * 32 * R * PW * 8;
+      if (R == 1)
+        k_far_sym_w<KT, 1><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+                                                   d_trans_, d_img_, mm, up, kp, down, sl);
+      else if (R == 2)
+        k_far_sym_w<KT, 2><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+                                                   d_trans_, d_img_, mm, up, kp, down, sl);
+      else if (R == 3)
+        k_far_sym_w<KT, 3><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+                                                   d_trans_, d_img_, mm, up, kp, down, sl);
+      else
+        k_far_sym_w<KT, 4><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+                                                   d_trans_, d_img_, mm, up, kp, down, sl);
+      ++launches;
+      const int stride = rows * static_cast<int>(sizeof(S) / 8);
+      k_far_lower<false><<<grid_for(static_cast<long long>(P.n_nodes) * stride, 256), 256, 0, s>>>(
+          P.n_nodes, stride, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, reinterpret_cast<double*>(down));
     } else {
       KParams kp;
       kp.kr = as_.kp[0];

@@ -134,7 +134,8 @@ class H2Device {
   int *d_near_a_ = nullptr, *d_near_b_ = nullptr, *d_near_rs_ = nullptr;
   int *d_far_b_ = nullptr, *d_far_rs_ = nullptr, *d_far_targets_ = nullptr;
   int n_far_targets_ = 0;
-  bool sym_far_ = false;
+  bool sym_far_ = false;  // Laplace m <= 6: lane-tile symmetric far kernel
+  bool sym_w_ = false;    // other kinds / m, one GPU: warp-row symmetric far kernel
   int n_sym_targets_ = 0;
   int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;
   int n_sym_fine_ = 0, n_sym_coarse_ = 0;  // leaf-level / coarser symmetric targets
