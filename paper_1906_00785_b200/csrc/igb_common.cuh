@@ -118,17 +118,27 @@ struct MaxT {
 
 // Green's functions (operators.hpp:16-20), distance clamped as in
 // pair_integration.hpp:18,118
+// Branch-free FP64 reciprocal square root for normal positive inputs:
+// MUFU.RSQ64H seed (rsqrt.approx.ftz.f64, rel. err < 2^-22) + 2 Newton steps.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  // one cubic (Householder) step: y = y0 (1 + e/2 + 3e^2/8), e = 1 - x y0^2
+  const double e = fma(-x * y0, y0, 1.0);
+  return fma(y0 * e, fma(0.375, e, 0.5), y0);
+}
+
+// G(max(r, 1e-14)) (operators.hpp:16-20, pair_integration.hpp:22-28); 1/r from
+// the refined reciprocal square root (~1 ulp), r = r^2 / r
 __device__ __forceinline__ double green(double r2, const KParams&, double) {
-  double rinv = rsqrt(r2);
-  if (r2 < 1e-28) rinv = 1e14;
-  return rinv * kInv4Pi;
+  return rsqrt_nr(fmax(r2, 1e-28)) * kInv4Pi;
 }
 __device__ __forceinline__ cd green_c(double r2, const KParams& kp) {
-  double r = sqrt(r2);
-  r = fmax(r, 1e-14);
+  const double r2c = fmax(r2, 1e-28);
+  const double ir = rsqrt_nr(r2c), r = r2c * ir;
   double s, c;
   sincos(kp.kr * r, &s, &c);
-  double a = kInv4Pi / r;
+  double a = kInv4Pi * ir;
   if (kp.ki != 0.0) a *= exp(kp.ki * r);
   return mk(a * c, -a * s);
 }

@@ -1095,15 +1095,6 @@ __global__ void __launch_bounds__(256) k_far_sym_w(int n_targets, const int* __r
   }
 }
 
-// Branch-free FP64 reciprocal square root for normal positive inputs:
-// MUFU.RSQ64H seed (rsqrt.approx.ftz.f64, rel. err < 2^-22) + 2 Newton steps.
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y0;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
-  // one cubic (Householder) step: y = y0 (1 + e/2 + 3e^2/8), e = 1 - x y0^2
-  const double e = fma(-x * y0, y0, 1.0);
-  return fma(y0 * e, fma(0.375, e, 0.5), y0);
-}
 
 template <int M>
 struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
