@@ -2352,7 +2352,7 @@ void H2Device::dist_phase1(const double* x, double* send, cudaStream_t s) {
   }
   IGB_CUDA(cudaMemcpyAsync(dx_, x, static_cast<size_t>(dim()) * sw, cudaMemcpyDeviceToDevice, s));
   IGB_CUDA(cudaGraphLaunch(graph1_, s));
-  if (send_count() > 0 && send != nullptr)
+  if (lp_.world > 1 && send_count() > 0 && send != nullptr)  // one rank: nothing is exchanged
     IGB_CUDA(cudaMemcpyAsync(send, d_send_, send_count() * sw, cudaMemcpyDeviceToDevice, s));
 }
 void H2Device::dist_phase2(const double* recv, double* y, cudaStream_t s) {
