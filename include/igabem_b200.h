@@ -102,7 +102,7 @@ int igb_h2_create(const igb_discretization* d, const igb_h2_opts* opts, int devi
 /* flags for igb_h2_create_ex: IGB_H2_STORED_COUPLINGS keeps the far couplings
  * in HBM in the reference format (h2.cpp:218-229); the default evaluates them
  * on the fly inside the matvec (same values, no coupling storage) */
-enum { IGB_H2_STORED_COUPLINGS = 2 };
+enum { IGB_H2_STORED_COUPLINGS = 2, IGB_H2_DEVICE_PARTITION = 4 };
 int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, igb_h2** out);
 /* ---- multi-GPU row-cluster partition ----
  * rank `rank` of `world` assembles and applies the block rows of its level-1
@@ -181,6 +181,10 @@ void igb_h2_destroy(igb_h2* h);
  * traversal and pair classification of H2Matrix (h2.cpp:49-97,175-252) ---- */
 typedef struct igb_plan igb_plan;
 int igb_plan_create(const igb_discretization* d, const igb_h2_opts* opts, igb_plan** out);
+/* flags & IGB_H2_DEVICE_PARTITION (also for igb_h2_create_ex): the traversal,
+   sort, row starts and transposes of the block partition run on CUDA device
+   `device` (the lists are bit-identical to the host's) */
+int igb_plan_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int flags, int device, igb_plan** out);
 int igb_plan_counts(const igb_plan* p, long long* n_near, long long* n_far, int* n_nodes);
 int igb_plan_near_pairs(const igb_plan* p, int* out);
 int igb_plan_far_pairs(const igb_plan* p, int* out);

@@ -457,6 +457,17 @@ int igb_plan_create(const igb_discretization* d, const igb_h2_opts* opts, igb_pl
     *out = p.release();
   });
 }
+int igb_plan_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int flags, int device, igb_plan** out) {
+  return guard([&] {
+    need(d, "discretization");
+    need(out, "out");
+    igb_h2_opts o = opts ? *opts : igb_h2_opts{8, 1.6, 0, 0};
+    auto p = std::make_unique<igb_plan>();
+    p->d = d->d;
+    p->plan = igb::build_plan(*d->d, o.m, o.eta, o.far_order, o.sing_order, (flags & 4) ? device : -1);
+    *out = p.release();
+  });
+}
 int igb_plan_counts(const igb_plan* p, long long* n_near, long long* n_far, int* n_nodes) {
   return guard([&] {
     need(p, "plan");

@@ -1594,7 +1594,7 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   lap("stage 1 launched");
   // ---- stage 2: block partition on the host, overlapping the device
   const auto t0 = std::chrono::steady_clock::now();
-  plan_ = build_plan(d, opt_.m, opt_.eta, opt_.far_order, opt_.sing_order);
+  plan_ = build_plan(d, opt_.m, opt_.eta, opt_.far_order, opt_.sing_order, (flags_ & 4) ? device_ : -1);
   lp_ = build_local_plan(d, plan_, opt_.world, opt_.rank);
   times_.plan_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   lap("plan");

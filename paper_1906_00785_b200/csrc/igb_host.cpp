@@ -1062,7 +1062,7 @@ void check_h2_options(const Discretization& d, int m, double eta, int far_order,
   if (*nfar > 64 || *nsing > 64) throw std::invalid_argument("gauss_rule: order out of range");
 }
 
-H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order) {
+H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order, int partition_device) {
   static const bool verbose = getenv("IGB_VERBOSE") != nullptr;
   auto tp = std::chrono::steady_clock::now();
   auto lap = [&](const char* what) {
@@ -1117,6 +1117,10 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
   // undecided level-2 pairs are traversed in parallel (balanced work list).
   std::vector<double> diag(nn);
   for (int i = 0; i < nn; ++i) diag[i] = P.node_box[i].diag_norm();
+  if (partition_device >= 0) {
+    device_partition(P, d, diag, eta, partition_device);
+    lap("device partition");
+  } else {
   auto child = [&](int node, int k) {
     return static_cast<int>(P.node_id(P.node_patch[node], P.node_level[node] + 1, 2 * P.node_sx[node] + (k & 1),
                                       2 * P.node_sy[node] + (k >> 1)));
@@ -1219,7 +1223,6 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
   bucket(far_parts, nn, P.far_a, P.far_b, P.far_row_start);
   bucket(near_parts, ne, P.near_a, P.near_b, P.near_row_start);
   lap("sort");
-  const long long nnear = static_cast<long long>(P.near_a.size());
   const long long nfar_pairs = static_cast<long long>(P.far_a.size());
   lap("row starts");
   // symmetric structure of the admissible pairs: (t, s) <-> (s, t).  Pairs
@@ -1245,6 +1248,8 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
   }
   if (asym) throw std::logic_error("B200 H2: admissible relation is not symmetric");
   lap("transposes");
+  }  // host partition
+  const long long nnear = static_cast<long long>(P.near_a.size());
   // classification + unique singular work lists
   P.near_cls.resize(nnear);
   std::vector<uint8_t> mapa(nnear), mapb(nnear);

@@ -246,7 +246,13 @@ struct H2Plan {
     return static_cast<long long>(p) * npp + level_offset[l] + sx + (1LL << l) * sy;
   }
 };
-H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order);
+// partition_device >= 0: the traversal, sort, row starts, upper starts and
+// transposes run on that CUDA device (device_partition, bit-identical lists)
+H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int sing_order,
+                  int partition_device = -1);
+// fills near_a/b, near_row_start, far_a/b, far_row_start, far_upper_start,
+// far_trans of P (tree and node boxes already built); igb_plan_gpu.cu
+void device_partition(H2Plan& P, const Discretization& d, const std::vector<double>& diag, double eta, int device);
 // Option checks of build_plan (h2.hpp:60 ctor) and the quadrature orders it
 // derives (far: degree + 2, singular: degree + 3 unless given).
 void check_h2_options(const Discretization& d, int m, double eta, int far_order, int sing_order, int* nfar,

@@ -88,7 +88,7 @@ SYMBOLS = (
     "igb_h2_moments", "igb_h2_images", "igb_h2_assembly_times", "igb_h2_device_bytes", "igb_h2_bench_apply",
     "igb_h2_gmres", "igb_h2_cg", "igb_rhs_points", "igb_rhs_assemble", "igb_potential", "igb_dense_assemble",
     "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
-    "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_counts", "igb_plan_near_pairs",
+    "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_create_ex", "igb_plan_counts", "igb_plan_near_pairs",
     "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
     "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
 )
@@ -151,6 +151,7 @@ def lib():
     L.igb_h2_destroy.argtypes = [vp]
     L.igb_h2_destroy.restype = None
     L.igb_plan_create.argtypes = [vp, P(_Opts), P(vp)]
+    L.igb_plan_create_ex.argtypes = [vp, P(_Opts), i32, i32, P(vp)]
     L.igb_plan_counts.argtypes = [vp, P(i64), P(i64), P(i32)]
     L.igb_plan_near_pairs.argtypes = [vp, P(i32)]
     L.igb_plan_far_pairs.argtypes = [vp, P(i32)]
@@ -365,14 +366,18 @@ def admissible(box_a, box_b, eta):
 
 
 class H2Plan:
-    """Host-only block partition of H2Matrix (cluster tree, admissibility
-    traversal, pair classification; h2.cpp:49-97,175-252) -- no device."""
+    """Block partition of H2Matrix (cluster tree, admissibility traversal, pair
+    classification; h2.cpp:49-97,175-252).  device=None: all on the host;
+    device=k: traversal, sort and transposes on CUDA device k (bit-identical)."""
 
-    def __init__(self, disc: Discretization, opts: H2Options | None = None):
+    def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int | None = None):
         opts = opts or H2Options()
         o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
         h = ctypes.c_void_p()
-        _check(lib().igb_plan_create(disc._h, ctypes.byref(o), ctypes.byref(h)))
+        if device is None:
+            _check(lib().igb_plan_create(disc._h, ctypes.byref(o), ctypes.byref(h)))
+        else:
+            _check(lib().igb_plan_create_ex(disc._h, ctypes.byref(o), 4, int(device), ctypes.byref(h)))
         self._h = h
         a, b, c = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_int()
         _check(lib().igb_plan_counts(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
@@ -430,11 +435,11 @@ class H2Matrix:
     complex128 for Helmholtz / Maxwell), like the reference's Eigen vectors."""
 
     def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int = 0,
-                 stored_couplings: bool = False, world: int = 1, rank: int = 0):
+                 stored_couplings: bool = False, world: int = 1, rank: int = 0, device_partition: bool = False):
         opts = opts or H2Options()
         o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
         h = ctypes.c_void_p()
-        flags = 2 if stored_couplings else 0
+        flags = (2 if stored_couplings else 0) | (4 if device_partition else 0)
         if world == 1:
             _check(lib().igb_h2_create_ex(disc._h, ctypes.byref(o), int(device), flags, ctypes.byref(h)))
         else:
