@@ -76,6 +76,12 @@ __device__ __forceinline__ double shfl_xor(double v, int o) { return __shfl_xor_
 __device__ __forceinline__ cd shfl_xor(cd v, int o) {
   return mk(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
 }
+// programmatic dependent launch: allow the next kernel of the stream to launch,
+// then wait for this kernel's predecessors (no-ops when launched without PDL)
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 __device__ __forceinline__ double ldg_s(const double* p) { return __ldg(p); }
 __device__ __forceinline__ cd ldg_s(const cd* p) {
   const double2 v = __ldg(reinterpret_cast<const double2*>(p));

@@ -698,7 +698,8 @@ __global__ void __launch_bounds__(128) k_sing_scatter(const int* __restrict__ sl
 // --------------------------------------------------------- K6: matvec
 template <class S>
 __global__ void k_coef(int n, const S* __restrict__ x, const int* __restrict__ l2g, const double* __restrict__ sg,
-                       S* __restrict__ coef) {  // h2.cpp:271-279
+                       S* __restrict__ coef) {
+  pdl_entry();  // h2.cpp:271-279
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) coef[i] = x[l2g[i]] * sg[i];
 }
@@ -707,7 +708,8 @@ __device__ __forceinline__ double operator_mul(double a, double b) { return a * 
 template <class S, int NL>
 __global__ void k_leaf_up(int n_el, const int* __restrict__ el, int rows, int epp, int npp, int leaf_off,
                           const double* __restrict__ mom, const S* __restrict__ coef,
-                          S* __restrict__ up) {  // h2.cpp:281-290, owned leaves
+                          S* __restrict__ up) {
+  pdl_entry();  // h2.cpp:281-290, owned leaves
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n_el) * rows) return;
   const int e = el[idx / rows], r = static_cast<int>(idx % rows);
@@ -725,6 +727,7 @@ template <class S, int NL>
 __global__ void k_leaf_up_x(int n_el, int rows, int epp, int npp, int leaf_off, const double* __restrict__ mom,
                             const S* __restrict__ x, const int* __restrict__ l2g, const double* __restrict__ sg,
                             S* __restrict__ up, S* __restrict__ down, long long ndown) {
+  pdl_entry();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx < ndown) down[idx] = zero<S>();
   if (idx >= static_cast<long long>(n_el) * rows) return;
@@ -756,6 +759,7 @@ template <class S, int M>
 __global__ void k_up_level(int np, int level, int npp, int off_l, int off_c, int m_rt, int nch,
                            const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ up, int c0,
                            int c1) {
+  pdl_entry();
   const int m = M ? M : m_rt;
   const int mm = m * m, rows = nch * mm, nside = 1 << level;
   const int per = level == 0 ? 1 : (1 << (2 * (level - 1)));
@@ -1235,6 +1239,7 @@ __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs,
                             const int* __restrict__ far_b, const unsigned char* __restrict__ owned,
                             const double* __restrict__ slot, double* __restrict__ down, int rows = 0, int npp = 1,
                             int leaf_off = 0) {
+  pdl_entry();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n_nodes) * mm) return;
   const int s = static_cast<int>(idx / mm), nu = static_cast<int>(idx % mm);
@@ -1255,6 +1260,7 @@ template <class S, int M>
 __global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, int m_rt, int nch,
                              const double* __restrict__ tl, const double* __restrict__ tr, S* __restrict__ down,
                              int c0, int c1) {
+  pdl_entry();
   (void)np;
   const int m = M ? M : m_rt;
   const int mm = m * m, rows = nch * mm, cside = 2 << level, per = 1 << (2 * level);
@@ -1284,12 +1290,14 @@ __global__ void k_down_level(int np, int level, int npp, int off_p, int off_c, i
 // all-gather payload of the up moments (owned nodes, levels >= 1)
 template <class S>
 __global__ void k_pack(int n, const int* __restrict__ nodes, int rows, const S* __restrict__ up, S* __restrict__ send) {
+  pdl_entry();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n) * rows) return;
   send[idx] = up[static_cast<size_t>(nodes[idx / rows]) * rows + idx % rows];
 }
 template <class S>
 __global__ void k_unpack(int n, const int* __restrict__ nodes, int rows, const S* __restrict__ recv, S* __restrict__ up) {
+  pdl_entry();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n) * rows) return;
   const int node = nodes[idx / rows];
@@ -1352,6 +1360,7 @@ __global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restri
                                                    int leaf_off, const double* __restrict__ mom,
                                                    const S* __restrict__ down, const S* __restrict__ near_rows,
                                                    S* __restrict__ loc) {
+  pdl_entry();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n_el) * NL) return;
   const int i = static_cast<int>(idx / NL), l = static_cast<int>(idx % NL);
@@ -1368,6 +1377,7 @@ __global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restri
 template <class S>
 __global__ void k_scatter(int nd, const int* __restrict__ start, const int* __restrict__ inc,
                           const double* __restrict__ sg, const S* __restrict__ loc, S* __restrict__ y) {
+  pdl_entry();
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= nd) return;
   S acc = zero<S>();
@@ -1380,6 +1390,7 @@ __global__ void k_scatter(int nd, const int* __restrict__ start, const int* __re
 
 template <class S>
 __global__ void k_zero(size_t n, S* p) {
+  pdl_entry();
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (i < n) p[i] = zero<S>();
 }
@@ -1389,33 +1400,55 @@ __global__ void k_zero(size_t n, S* p) {
 // ====================================================== host driver
 using namespace dev;
 
+// Small, latency-bound kernels of the matvec chains are launched with
+// programmatic stream serialisation: a launch may become resident while its
+// predecessor finishes (each such kernel begins with pdl_entry()).
+#ifndef IGB_PDL
+#define IGB_PDL 1
+#endif
+template <class... KArgs, class... Args>
+static void pdl_launch(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = IGB_PDL ? 1 : 0;
+  IGB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 // transfer kernels with the interpolation degree as a template parameter
 template <class S, class... A>
 static void launch_up_level(unsigned grid, cudaStream_t s, A... a) {
   const int m = std::get<5>(std::make_tuple(a...));
   switch (m) {
-    case 2: k_up_level<S, 2><<<grid, 256, 0, s>>>(a...); break;
-    case 3: k_up_level<S, 3><<<grid, 256, 0, s>>>(a...); break;
-    case 4: k_up_level<S, 4><<<grid, 256, 0, s>>>(a...); break;
-    case 5: k_up_level<S, 5><<<grid, 256, 0, s>>>(a...); break;
-    case 6: k_up_level<S, 6><<<grid, 256, 0, s>>>(a...); break;
-    case 7: k_up_level<S, 7><<<grid, 256, 0, s>>>(a...); break;
-    case 8: k_up_level<S, 8><<<grid, 256, 0, s>>>(a...); break;
-    default: k_up_level<S, 0><<<grid, 256, 0, s>>>(a...); break;
+    case 2: pdl_launch(k_up_level<S, 2>, grid, 256, 0, s, a...); break;
+    case 3: pdl_launch(k_up_level<S, 3>, grid, 256, 0, s, a...); break;
+    case 4: pdl_launch(k_up_level<S, 4>, grid, 256, 0, s, a...); break;
+    case 5: pdl_launch(k_up_level<S, 5>, grid, 256, 0, s, a...); break;
+    case 6: pdl_launch(k_up_level<S, 6>, grid, 256, 0, s, a...); break;
+    case 7: pdl_launch(k_up_level<S, 7>, grid, 256, 0, s, a...); break;
+    case 8: pdl_launch(k_up_level<S, 8>, grid, 256, 0, s, a...); break;
+    default: pdl_launch(k_up_level<S, 0>, grid, 256, 0, s, a...); break;
   }
 }
 template <class S, class... A>
 static void launch_down_level(unsigned grid, cudaStream_t s, A... a) {
   const int m = std::get<5>(std::make_tuple(a...));
   switch (m) {
-    case 2: k_down_level<S, 2><<<grid, 256, 0, s>>>(a...); break;
-    case 3: k_down_level<S, 3><<<grid, 256, 0, s>>>(a...); break;
-    case 4: k_down_level<S, 4><<<grid, 256, 0, s>>>(a...); break;
-    case 5: k_down_level<S, 5><<<grid, 256, 0, s>>>(a...); break;
-    case 6: k_down_level<S, 6><<<grid, 256, 0, s>>>(a...); break;
-    case 7: k_down_level<S, 7><<<grid, 256, 0, s>>>(a...); break;
-    case 8: k_down_level<S, 8><<<grid, 256, 0, s>>>(a...); break;
-    default: k_down_level<S, 0><<<grid, 256, 0, s>>>(a...); break;
+    case 2: pdl_launch(k_down_level<S, 2>, grid, 256, 0, s, a...); break;
+    case 3: pdl_launch(k_down_level<S, 3>, grid, 256, 0, s, a...); break;
+    case 4: pdl_launch(k_down_level<S, 4>, grid, 256, 0, s, a...); break;
+    case 5: pdl_launch(k_down_level<S, 5>, grid, 256, 0, s, a...); break;
+    case 6: pdl_launch(k_down_level<S, 6>, grid, 256, 0, s, a...); break;
+    case 7: pdl_launch(k_down_level<S, 7>, grid, 256, 0, s, a...); break;
+    case 8: pdl_launch(k_down_level<S, 8>, grid, 256, 0, s, a...); break;
+    default: pdl_launch(k_down_level<S, 0>, grid, 256, 0, s, a...); break;
   }
 }
 
@@ -2004,7 +2037,7 @@ void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, c
   };
   mark(0);
   const int nloc = ne * NL;
-  k_coef<S><<<grid_for(nloc, 256), 256, 0, s>>>(nloc, x, d_l2g_, d_lsign_, coef);
+  pdl_launch(k_coef<S>, grid_for(nloc, 256), 256, 0, s, nloc, x, d_l2g_, d_lsign_, coef);
   ++launches;
   mark(1);
   // near-field rows (HBM-bound) run on a forked stream, overlapping the
@@ -2018,7 +2051,7 @@ void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, c
     ++launches;
     IGB_CUDA(cudaEventRecord(ev_join_, side_));
   }
-  k_leaf_up<S, NL><<<grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s>>>(
+  pdl_launch(k_leaf_up<S, NL>, grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s, 
       nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, coef, up);
   ++launches;
   mark(2);
@@ -2030,7 +2063,7 @@ void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, c
   }
   if (Lp.world > 1 && Lp.pack_nodes.size()) {
     const long long tot = static_cast<long long>(Lp.pack_nodes.size()) * rows;
-    k_pack<S><<<grid_for(tot, 256), 256, 0, s>>>(static_cast<int>(Lp.pack_nodes.size()), d_pack_nodes_, rows, up,
+    pdl_launch(k_pack<S>, grid_for(tot, 256), 256, 0, s, static_cast<int>(Lp.pack_nodes.size()), d_pack_nodes_, rows, up,
                                                   reinterpret_cast<S*>(send ? send : d_send_));
     ++launches;
   }
@@ -2068,7 +2101,7 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
   }
   if (Lp.world > 1) {
     const long long tot = static_cast<long long>(Lp.world) * Lp.pack_max * rows;
-    k_unpack<S><<<grid_for(tot, 256), 256, 0, s>>>(Lp.world * Lp.pack_max, d_unpack_nodes_, rows,
+    pdl_launch(k_unpack<S>, grid_for(tot, 256), 256, 0, s, Lp.world * Lp.pack_max, d_unpack_nodes_, rows,
                                                     reinterpret_cast<const S*>(recv ? recv : d_recv_), up);
     ++launches;
   }
@@ -2080,7 +2113,7 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
   }
   mark(3);
   const size_t ndown = static_cast<size_t>(P.n_nodes) * rows;
-  k_zero<S><<<grid_for(static_cast<long long>(ndown), 256), 256, 0, s>>>(ndown, down);
+  pdl_launch(k_zero<S>, grid_for(static_cast<long long>(ndown), 256), 256, 0, s, ndown, down);
   ++launches;
   mark(4);
   if (n_far_targets_ > 0) {
@@ -2126,11 +2159,11 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
 #undef IGB_FS
       ++launches;
       if (lp_.world > 1)
-        k_far_lower<true><<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(
-            P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn);
+        pdl_launch(k_far_lower<true>, grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s, 
+            P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn, 0, 1, 0);
       else
-        k_far_lower<false><<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s>>>(
-            P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn);
+        pdl_launch(k_far_lower<false>, grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s, 
+            P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn, 0, 1, 0);
     } else if (sym_w_) {
       KParams kp;
       kp.kr = as_.kp[0];
@@ -2156,8 +2189,8 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
                                                    d_trans_, d_img_, mm, up, kp, down, sl);
       ++launches;
       const int stride = rows * static_cast<int>(sizeof(S) / 8);
-      k_far_lower<false><<<grid_for(static_cast<long long>(P.n_nodes) * stride, 256), 256, 0, s>>>(
-          P.n_nodes, stride, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, reinterpret_cast<double*>(down));
+      pdl_launch(k_far_lower<false>, grid_for(static_cast<long long>(P.n_nodes) * stride, 256), 256, 0, s, 
+          P.n_nodes, stride, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, reinterpret_cast<double*>(down), 0, 1, 0);
     } else {
       KParams kp;
       kp.kr = as_.kp[0];
@@ -2192,11 +2225,11 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
     ++launches;
   }
   if (pev == nullptr) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));  // near rows (side stream) done
-  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s>>>(
+  pdl_launch(k_leaf_down<S, NL>, grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s, 
       nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
   ++launches;
   mark(7);
-  k_scatter<S><<<grid_for(d.dof_count(), 256), 256, 0, s>>>(d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
+  pdl_launch(k_scatter<S>, grid_for(d.dof_count(), 256), 256, 0, s, d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
   ++launches;
   mark(8);
   IGB_CUDA(cudaGetLastError());
@@ -2245,7 +2278,7 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   ++launches;
   IGB_CUDA(cudaEventRecord(ev_join_, side_));
   const long long ndown = static_cast<long long>(P.n_nodes) * rows;
-  k_leaf_up_x<S, NL><<<grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s>>>(
+  pdl_launch(k_leaf_up_x<S, NL>, grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s, 
       nel, rows, epp, npp, P.level_offset[L], d_mom_, x, d_l2g_, d_lsign_, up, down, ndown);
   ++launches;
   IGB_CUDA(cudaEventRecord(ev_fork2_, s));
@@ -2263,7 +2296,7 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
     ++launches;
   };
   auto far_lower = [&](cudaStream_t st, int which) {
-    k_far_lower<false><<<grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, st>>>(
+    pdl_launch(k_far_lower<false>, grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, st, 
         P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn, which, npp, P.level_offset[L]);
     ++launches;
   };
@@ -2295,9 +2328,9 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
     ++launches;
   }
   IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
-  k_leaf_down<S, NL><<<grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s>>>(
+  pdl_launch(k_leaf_down<S, NL>, grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s, 
       nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
-  k_scatter<S><<<grid_for(d.dof_count(), 256), 256, 0, s>>>(d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
+  pdl_launch(k_scatter<S>, grid_for(d.dof_count(), 256), 256, 0, s, d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
   launches += 2;
   IGB_CUDA(cudaGetLastError());
   apply_launches_ = launches;
