@@ -485,7 +485,10 @@ struct SingLayout {
   static constexpr int STAGE = CH * STR * (SW + 1);
   static constexpr int RED = SL * NL * NL * SW;
   static constexpr int BODY = STAGE > RED ? STAGE : RED;
-  static constexpr int LMAX = 32;               // rule lines per chunk (setup capacity)
+#ifndef IGB_SING_LMAX
+#define IGB_SING_LMAX 16  // 8 setup tasks per line: one round of 128 threads
+#endif
+  static constexpr int LMAX = IGB_SING_LMAX;    // rule lines per chunk (setup capacity)
   // real kernels with up to 9 local functions fit 128 registers: 4 CTAs / SM
 #ifndef IGB_SING_MINB
 #define IGB_SING_MINB 4
