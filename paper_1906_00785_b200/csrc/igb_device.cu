@@ -566,10 +566,12 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   const int lpc = min(LY::LMAX, CH / n), cpts = lpc * n;
   const float rn = 1.0f / static_cast<float>(n);
   const int my_ll = div_n(tid, n, rn), my_k = tid - my_ll * n;  // this thread's point of a chunk
-  for (int lbase = 0; lbase < nlines; lbase += lpc) {
+  // phases per chunk: point evaluation | GEMM of this chunk + setup of the next
+  // (disjoint shared regions), two barriers per chunk
+  auto do_setup = [&](int lb) {
     for (int task = tid; task < lpc * 8; task += 128) {
       const int ll = task >> 3, e = (task >> 2) & 1, c = task & 3;
-      const int line = lbase + ll;
+      const int line = lb + ll;
       if (line < nlines) {
         double c0[4], c1[4], wl;
         rule_line<CLS>(line, n, rn, gx, gw, ma, mb, c0, c1, wl);
@@ -589,7 +591,10 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
         }
       }
     }
-    __syncthreads();
+  };
+  do_setup(0);
+  __syncthreads();
+  for (int lbase = 0; lbase < nlines; lbase += lpc) {
     if (tid < cpts) {
       const int p = lbase * n + tid;
       S* ga = Ga + tid * STR;
@@ -654,6 +659,7 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
         }
       }
     }
+    if (lbase + lpc < nlines) do_setup(lbase + lpc);
     __syncthreads();
   }
   S* red = reinterpret_cast<S*>(body);
