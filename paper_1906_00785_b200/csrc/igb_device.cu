@@ -1827,11 +1827,20 @@ void H2Device::stage_plan() {
       std::vector<int> sym_targets;
       for (int t : Lp.far_targets)
         if (Lp.world > 1 || P.far_upper_start[t] < P.far_row_start[t + 1]) sym_targets.push_back(t);
-      // longest rows first (one warp per target): the last wave holds the light rows
-      auto work = [&](int t) {
-        return Lp.world > 1 ? P.far_row_start[t + 1] - P.far_row_start[t] : P.far_row_start[t + 1] - P.far_upper_start[t];
-      };
-      std::stable_sort(sym_targets.begin(), sym_targets.end(), [&](int a, int b) { return work(a) > work(b); });
+      // longest rows first (one warp per target): the last wave holds the light
+      // rows.  The lane-tile kernel (little work per pair) only while the
+      // source data (node images + moments) sits in L2: beyond that node order
+      // keeps neighbouring targets, which share source clusters, in
+      // neighbouring warps (c5: 15.1 vs 16.7 ms per far field); the warp-row
+      // kernel (m^4 complex evaluations per pair) always (c3: 82.9 vs 85.5 ms)
+      const double src_bytes = static_cast<double>(P.n_nodes) * mm * (3 + nch_ * sw) * 8.0;
+      if (sym_w_ || src_bytes <= 64.0 * (1 << 20)) {
+        auto work = [&](int t) {
+          return Lp.world > 1 ? P.far_row_start[t + 1] - P.far_row_start[t]
+                              : P.far_row_start[t + 1] - P.far_upper_start[t];
+        };
+        std::stable_sort(sym_targets.begin(), sym_targets.end(), [&](int a, int b) { return work(a) > work(b); });
+      }
       n_sym_targets_ = static_cast<int>(sym_targets.size());
       d_sym_targets_ = upload(sym_targets);
       std::vector<int> fine, coarse;
