@@ -1113,9 +1113,16 @@ template <int M>
 struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static constexpr int MM = M * M;
   // m = 4: 4 x 8 lanes (A/B on B200: 0.37 ms vs 0.41 ms for 2 x 16 at c2);
-  // m = 5: 2 x 16 (no spills at 1 block/SM)
-  static constexpr int BR = (M == 5) ? 2 : (M == 3 ? 3 : 4);
-  static constexpr int BC = (M == 5) ? 16 : (M == 2 ? 4 : (M == 3 ? 9 : 8));
+  // m = 5: 5 x 6 lanes, an exact 5 x 5 tile each (30 of 32 lanes)
+#ifndef IGB_M5_MINB
+#define IGB_M5_MINB 2
+#endif
+#ifndef IGB_M5_BR
+#define IGB_M5_BR 5
+#define IGB_M5_BC 6
+#endif
+  static constexpr int BR = (M == 5) ? IGB_M5_BR : (M == 3 ? 3 : 4);
+  static constexpr int BC = (M == 5) ? IGB_M5_BC : (M == 2 ? 4 : (M == 3 ? 9 : 8));
   static constexpr int RN = (MM + BR - 1) / BR, CN = (MM + BC - 1) / BC;
   static_assert(BR * BC <= 32, "lane grid");
 };
@@ -2171,7 +2178,7 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
         case 2: IGB_FS(2, 3); break;
         case 3: IGB_FS(3, 3); break;
         case 4: IGB_FS(4, 3); break;
-        case 5: IGB_FS(5, 1); break;
+        case 5: IGB_FS(5, IGB_M5_MINB); break;
         default: IGB_FS(6, 1); break;
       }
 #undef IGB_FS
@@ -2308,7 +2315,7 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
       case 2: k_far_sym<2, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
       case 3: k_far_sym<3, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
       case 4: k_far_sym<4, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
-      case 5: k_far_sym<5, false, 1><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
+      case 5: k_far_sym<5, false, IGB_M5_MINB><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
       default: k_far_sym<6, false, 1><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
     }
     ++launches;
