@@ -493,7 +493,10 @@ struct SingLayout {
 #ifndef IGB_SING_MINB
 #define IGB_SING_MINB 4
 #endif
-  static constexpr int MINB = (KT::KIND == 0 && NL <= 9) ? IGB_SING_MINB : 1;
+#ifndef IGB_SING_MINB16
+#define IGB_SING_MINB16 4
+#endif
+  static constexpr int MINB = (KT::KIND == 0 && NL <= 9) ? IGB_SING_MINB : (KT::KIND == 0 && NL <= 16 ? IGB_SING_MINB16 : 1);
   // per line: [element][component][A0..4, B0..4] (80), the affine rule
   // descriptor (c0, c1) x 4 + weight (9); odd stride (the lines of one warp
   // read distinct banks)
