@@ -496,7 +496,17 @@ struct SingLayout {
 #ifndef IGB_SING_MINB16
 #define IGB_SING_MINB16 4
 #endif
-  static constexpr int MINB = (KT::KIND == 0 && NL <= 9) ? IGB_SING_MINB : (KT::KIND == 0 && NL <= 16 ? IGB_SING_MINB16 : 1);
+#ifndef IGB_SING_MINBM
+#define IGB_SING_MINBM 1
+#endif
+#ifndef IGB_SING_MINBH
+#define IGB_SING_MINBH 4
+#endif
+  static constexpr int MINB = (KT::KIND == 0 && NL <= 9)    ? IGB_SING_MINB
+                              : (KT::KIND == 0 && NL <= 16) ? IGB_SING_MINB16
+                              : (KT::KIND == 1 && NL <= 9)  ? IGB_SING_MINBH
+                              : (KT::KIND == 2 && NL <= 12) ? IGB_SING_MINBM
+                                                            : 1;
   // per line: [element][component][A0..4, B0..4] (80), the affine rule
   // descriptor (c0, c1) x 4 + weight (9); odd stride (the lines of one warp
   // read distinct banks)
