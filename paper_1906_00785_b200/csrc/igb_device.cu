@@ -1127,6 +1127,9 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static constexpr int MM = M * M;
   // m = 4: 4 x 8 lanes (A/B on B200: 0.37 ms vs 0.41 ms for 2 x 16 at c2);
   // m = 5: 5 x 6 lanes, an exact 5 x 5 tile each (30 of 32 lanes)
+#ifndef IGB_M4_MINB
+#define IGB_M4_MINB 3
+#endif
 #ifndef IGB_M5_MINB
 #define IGB_M5_MINB 2
 #endif
@@ -1139,6 +1142,27 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static constexpr int RN = (MM + BR - 1) / BR, CN = (MM + BC - 1) / BC;
   static_assert(BR * BC <= 32, "lane grid");
 };
+
+#ifndef IGB_FAR_DOT
+#define IGB_FAR_DOT 0
+#endif
+#ifndef IGB_FAR_NEWTON
+#define IGB_FAR_NEWTON 1
+#endif
+#if IGB_FAR_NEWTON
+// 2/r from the MUFU estimate y0 and one Newton step y0 (3 - x y0^2) (the
+// factor 1/2 of the step folded into the final scale): relative error
+// 1.5 e0^2 for the estimate's e0
+__device__ __forceinline__ double far_rsqrt(double x) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  return y0 * fma(-x * y0, y0, 3.0);
+}
+constexpr double kFarScale = 0.5 * kInv4Pi;
+#else
+__device__ __forceinline__ double far_rsqrt(double x) { return rsqrt_nr(x); }
+constexpr double kFarScale = kInv4Pi;
+#endif
 
 // Symmetric fused far field (Laplace): each unordered admissible pair {t, s},
 // t < s, is evaluated once by the warp of t: K = G(|img_t[nu] - img_s[mu]|)
@@ -1161,6 +1185,15 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
   const int bi = lane % BR, bj = lane / BR;
   const bool act = bj < BC;
   double tx[RN][3], xt[RN], acc[RN];
+#if IGB_FAR_DOT
+  // distances in dot form about the target's first node c:
+  // r^2 = |a - c|^2 + |b - c|^2 - 2 (a - c).(b - c); the relative rounding error
+  // is bounded by ~eps ((|a-c| + |b-c|) / r)^2 <= eps (2 eta + 1)^2 on admissible
+  // pairs (diam <= eta dist), so K agrees with the difference form to ~1e-15
+  const double* pc = img + static_cast<size_t>(t) * MM * 3;
+  const double c0 = pc[0], c1 = pc[1], c2 = pc[2];
+  double at[RN];
+#endif
 #pragma unroll
   for (int i = 0; i < RN; ++i) {
     const int nu = bi + BR * i;
@@ -1169,6 +1202,15 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
     tx[i][0] = p[0];
     tx[i][1] = p[1];
     tx[i][2] = p[2];
+#if IGB_FAR_DOT
+    tx[i][0] -= c0;
+    tx[i][1] -= c1;
+    tx[i][2] -= c2;
+    at[i] = tx[i][0] * tx[i][0] + tx[i][1] * tx[i][1] + tx[i][2] * tx[i][2];
+    tx[i][0] *= -2.0;
+    tx[i][1] *= -2.0;
+    tx[i][2] *= -2.0;
+#endif
     xt[i] = ok ? up[static_cast<size_t>(t) * MM + nu] : 0.0;
     acc[i] = 0.0;
   }
@@ -1199,11 +1241,20 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
     }
     double sx[CN][3], xs[CN], ps[CN];
     load(q);
+#if IGB_FAR_DOT
+    double bs[CN];
+#endif
 #pragma unroll
     for (int j = 0; j < CN; ++j) {
       sx[j][0] = nsx[j][0];
       sx[j][1] = nsx[j][1];
       sx[j][2] = nsx[j][2];
+#if IGB_FAR_DOT
+      sx[j][0] -= c0;
+      sx[j][1] -= c1;
+      sx[j][2] -= c2;
+      bs[j] = sx[j][0] * sx[j][0] + sx[j][1] * sx[j][1] + sx[j][2] * sx[j][2];
+#endif
       xs[j] = nxs[j];
       ps[j] = 0.0;
     }
@@ -1211,8 +1262,13 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
     for (int i = 0; i < RN; ++i)
 #pragma unroll
       for (int j = 0; j < CN; ++j) {
+#if IGB_FAR_DOT
+        const double r2 = fma(tx[i][0], sx[j][0], fma(tx[i][1], sx[j][1], fma(tx[i][2], sx[j][2], at[i] + bs[j])));
+#else
         const double d0 = tx[i][0] - sx[j][0], d1 = tx[i][1] - sx[j][1], d2 = tx[i][2] - sx[j][2];
-        const double gk = rsqrt_nr(d0 * d0 + d1 * d1 + d2 * d2);  // 4 pi G
+        const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
+#endif
+        const double gk = far_rsqrt(r2);  // kFarScale * 4 pi G
         acc[i] = fma(gk, xs[j], acc[i]);
         ps[j] = fma(gk, xt[i], ps[j]);
       }
@@ -1233,7 +1289,7 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
 #pragma unroll
       for (int j = 0; j < CN; ++j) {
         const int mu = bj + BC * j;
-        if (mu < MM) dst[mu] = ps[j] * kInv4Pi;
+        if (mu < MM) dst[mu] = ps[j] * kFarScale;
       }
     }
   }
@@ -1252,7 +1308,7 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
 #pragma unroll
     for (int i = 0; i < RN; ++i) {
       const int nu = bi + BR * i;
-      if (nu < MM) down[static_cast<size_t>(t) * MM + nu] = acc[i] * kInv4Pi;
+      if (nu < MM) down[static_cast<size_t>(t) * MM + nu] = acc[i] * kFarScale;
     }
   }
 }
@@ -2190,7 +2246,7 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
       switch (m) {  // occupancy chosen so no variant spills (ptxas -warn-spills)
         case 2: IGB_FS(2, 3); break;
         case 3: IGB_FS(3, 3); break;
-        case 4: IGB_FS(4, 3); break;
+        case 4: IGB_FS(4, IGB_M4_MINB); break;
         case 5: IGB_FS(5, IGB_M5_MINB); break;
         default: IGB_FS(6, 1); break;
       }
@@ -2327,7 +2383,7 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
     switch (m) {
       case 2: k_far_sym<2, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
       case 3: k_far_sym<3, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
-      case 4: k_far_sym<4, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
+      case 4: k_far_sym<4, false, IGB_M4_MINB><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
       case 5: k_far_sym<5, false, IGB_M5_MINB><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
       default: k_far_sym<6, false, 1><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
     }
