@@ -1143,9 +1143,6 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static_assert(BR * BC <= 32, "lane grid");
 };
 
-#ifndef IGB_FAR_DOT
-#define IGB_FAR_DOT 0
-#endif
 #ifndef IGB_FAR_NEWTON
 #define IGB_FAR_NEWTON 1
 #endif
@@ -1185,15 +1182,6 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
   const int bi = lane % BR, bj = lane / BR;
   const bool act = bj < BC;
   double tx[RN][3], xt[RN], acc[RN];
-#if IGB_FAR_DOT
-  // distances in dot form about the target's first node c:
-  // r^2 = |a - c|^2 + |b - c|^2 - 2 (a - c).(b - c); the relative rounding error
-  // is bounded by ~eps ((|a-c| + |b-c|) / r)^2 <= eps (2 eta + 1)^2 on admissible
-  // pairs (diam <= eta dist), so K agrees with the difference form to ~1e-15
-  const double* pc = img + static_cast<size_t>(t) * MM * 3;
-  const double c0 = pc[0], c1 = pc[1], c2 = pc[2];
-  double at[RN];
-#endif
 #pragma unroll
   for (int i = 0; i < RN; ++i) {
     const int nu = bi + BR * i;
@@ -1202,15 +1190,6 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
     tx[i][0] = p[0];
     tx[i][1] = p[1];
     tx[i][2] = p[2];
-#if IGB_FAR_DOT
-    tx[i][0] -= c0;
-    tx[i][1] -= c1;
-    tx[i][2] -= c2;
-    at[i] = tx[i][0] * tx[i][0] + tx[i][1] * tx[i][1] + tx[i][2] * tx[i][2];
-    tx[i][0] *= -2.0;
-    tx[i][1] *= -2.0;
-    tx[i][2] *= -2.0;
-#endif
     xt[i] = ok ? up[static_cast<size_t>(t) * MM + nu] : 0.0;
     acc[i] = 0.0;
   }
@@ -1241,20 +1220,11 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
     }
     double sx[CN][3], xs[CN], ps[CN];
     load(q);
-#if IGB_FAR_DOT
-    double bs[CN];
-#endif
 #pragma unroll
     for (int j = 0; j < CN; ++j) {
       sx[j][0] = nsx[j][0];
       sx[j][1] = nsx[j][1];
       sx[j][2] = nsx[j][2];
-#if IGB_FAR_DOT
-      sx[j][0] -= c0;
-      sx[j][1] -= c1;
-      sx[j][2] -= c2;
-      bs[j] = sx[j][0] * sx[j][0] + sx[j][1] * sx[j][1] + sx[j][2] * sx[j][2];
-#endif
       xs[j] = nxs[j];
       ps[j] = 0.0;
     }
@@ -1262,12 +1232,8 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
     for (int i = 0; i < RN; ++i)
 #pragma unroll
       for (int j = 0; j < CN; ++j) {
-#if IGB_FAR_DOT
-        const double r2 = fma(tx[i][0], sx[j][0], fma(tx[i][1], sx[j][1], fma(tx[i][2], sx[j][2], at[i] + bs[j])));
-#else
         const double d0 = tx[i][0] - sx[j][0], d1 = tx[i][1] - sx[j][1], d2 = tx[i][2] - sx[j][2];
         const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
-#endif
         const double gk = far_rsqrt(r2);  // kFarScale * 4 pi G
         acc[i] = fma(gk, xs[j], acc[i]);
         ps[j] = fma(gk, xt[i], ps[j]);
