@@ -425,10 +425,11 @@ def run_dist(args, c, name, igb, torch, dist, disc, opts, world, rank, dev):
 
 
 def singular_points(h, c):
-    """quadrature points executed per singular class (unique pairs x rule size)"""
+    """quadrature points executed per singular class (unique pairs x rule size;
+    coincident items run half the 8 n^4 rule and add the transpose)"""
     n4 = (c["P"] + 3) ** 4
     cc = h.class_counts()
-    return {"coincident": cc["coincident"] * 8 * n4, "edge": cc["edge"] * 6 * n4, "vertex": cc["vertex"] * 4 * n4}
+    return {"coincident": cc["coincident"] * 4 * n4, "edge": cc["edge"] * 6 * n4, "vertex": cc["vertex"] * 4 * n4}
 
 
 def flops_per_point(c, disc):

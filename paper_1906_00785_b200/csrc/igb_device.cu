@@ -393,7 +393,7 @@ __device__ __forceinline__ int div_n(int x, int n, float rn) {
 // maps of quadrature.hpp:25-29 folded in).
 template <int CLS>
 __device__ __forceinline__ void rule_line(int line, int n, float rn, const double* gx, const double* gw, int ma,
-                                          int mb, double c0[4], double c1[4], double& wl) {
+                                          int mb, double c0[4], double c1[4], double& wl, bool half = false) {
   int q = div_n(line, n, rn);
   const int i3 = line - q * n;
   int r = q;
@@ -405,8 +405,12 @@ __device__ __forceinline__ void rule_line(int line, int n, float rn, const doubl
   const int sec = q;
   const double w3 = gw[i1] * gw[i2] * gw[i3];
   if constexpr (CLS == 3) {  // coincident (quadrature.cpp:82-111)
-    const int axis = sec >> 2;
-    const double dir = (sec & 2) ? -1.0 : 1.0, sgn = (sec & 1) ? -1.0 : 1.0;
+    // half rule: only the dir = +1 sectors {0, 1, 4, 5}; (dir, sgn) -> (-dir,
+    // -sgn) maps z -> -z and swaps the two points with the same weight, so
+    // the other four sectors contribute the transpose (added at the end)
+    const int sec_ = half ? (((sec >> 1) << 2) | (sec & 1)) : sec;
+    const int axis = sec_ >> 2;
+    const double dir = (sec_ & 2) ? -1.0 : 1.0, sgn = (sec_ & 1) ? -1.0 : 1.0;
     const double t = gx[i1], s = gx[i2];
     double z1, z2;
     if (axis == 0) {
@@ -560,7 +564,11 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   const double sxb = ixb * h - cfb[100], syb = iyb * h - cfb[101];
   const double h4 = h * h * h * h;
   const int n4 = n * n * n * n;
-  const int npts = (CLS == 3 ? 8 : (CLS == 2 ? 6 : 4)) * n4;
+  // coincident items (same element, equal maps): the integrand is symmetric
+  // under exchanging the two points, so half the sectors give C and the block
+  // is C + C^T (the Galerkin symmetry the reference tests, test_assembly.cpp:20-29)
+  const bool half = CLS == 3 && ma == mb;
+  const int npts = (CLS == 3 ? (half ? 4 : 8) : (CLS == 2 ? 6 : 4)) * n4;
 
   S acc[TS][TS];
 #pragma unroll
@@ -587,7 +595,7 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
       const int line = lb + ll;
       if (line < nlines) {
         double c0[4], c1[4], wl;
-        rule_line<CLS>(line, n, rn, gx, gw, ma, mb, c0, c1, wl);
+        rule_line<CLS>(line, n, rn, gx, gw, ma, mb, c0, c1, wl, half);
         // the moving parameter of element e is the one with c1 != 0
         const int vm = e ? (c1[3] != 0.0) : (c1[1] != 0.0);
         const double sx0 = e ? sxb : sxa, sy0 = e ? syb : sya;
@@ -687,6 +695,11 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   for (int o = tid; o < NL * NL; o += 128) {
     S v = zero<S>();
     for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + o];
+    if (half) {
+      const int ot = (o % NL) * NL + o / NL;
+#pragma unroll 1
+      for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + ot];
+    }
     out[o] = v;
   }
 }
