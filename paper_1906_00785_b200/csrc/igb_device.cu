@@ -331,12 +331,15 @@ __global__ void k_dense_rows(int n_rows, const int* __restrict__ rows, int nd, c
 // (ea <= eb) writing the compact block, which k_sing_scatter places in the
 // two ordered slots (pair_integration.hpp:139-148).
 
+#ifndef IGB_SING_VEC
+#define IGB_SING_VEC 1
+#endif
 // Sum-factorised geometry jet.  Setup (once per rule line, element, homogeneous
 // component): with the fixed cell coordinate f, A_o = sum_k c[o][k] f^k and
 // B_o its derivative in f (the inner Horner loops of jet<4>); for a moving v
 // the coefficients are read as c[j][i] (o = j), for a moving u as c[i][j].
-__device__ __forceinline__ void jet_setup(const double* __restrict__ comp, int v_moves, double f,
-                                          double* __restrict__ out) {
+__device__ __forceinline__ void jet_setup_regs(const double* __restrict__ comp, int v_moves, double f,
+                                               double res[10]) {
   const int so = v_moves ? 5 : 1, sk = v_moves ? 1 : 5;
 #pragma unroll
   for (int o = 0; o <= kMaxGeomDeg; ++o) {
@@ -346,29 +349,41 @@ __device__ __forceinline__ void jet_setup(const double* __restrict__ comp, int v
       rp = fma(rp, f, r);
       r = fma(r, f, comp[o * so + k * sk]);
     }
-    out[o] = r;
-    out[5 + o] = rp;
+    res[o] = r;
+    res[5 + o] = rp;
   }
 }
-// Point of a line from its setup at the moving coordinate y: the outer Horner
-// loop of jet<4> (the same arithmetic when v moves) and the rational quotient.
-__device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_moves, double y, double x[3],
-                                         double du[3], double dv[3]) {
-  double N[4], Ns[4], Nt[4];
+__device__ __forceinline__ void jet_setup(const double* __restrict__ comp, int v_moves, double f,
+                                          double* __restrict__ out) {
+  double res[10];
+  jet_setup_regs(comp, v_moves, f, res);
+#if IGB_SING_VEC
+  double2* o2 = reinterpret_cast<double2*>(out);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const double* A = st + c * 10;
-    double n = 0.0, ny = 0.0, nx = 0.0;
+  for (int k = 0; k < 5; ++k) o2[k] = make_double2(res[2 * k], res[2 * k + 1]);
+#else
 #pragma unroll
-    for (int o = kMaxGeomDeg; o >= 0; --o) {
-      ny = fma(ny, y, n);
-      n = fma(n, y, A[o]);
-      nx = fma(nx, y, A[5 + o]);
-    }
-    N[c] = n;
-    Ns[c] = v_moves ? nx : ny;
-    Nt[c] = v_moves ? ny : nx;
+  for (int k = 0; k < 10; ++k) out[k] = res[k];
+#endif
+}
+// One homogeneous component at the moving coordinate y: the outer Horner loop
+// of jet<4> (the same arithmetic when v moves) -> value and the two partials.
+__device__ __forceinline__ void jet_comp(const double A[10], int v_moves, double y, double& N, double& Ns,
+                                         double& Nt) {
+  double n = 0.0, ny = 0.0, nx = 0.0;
+#pragma unroll
+  for (int o = kMaxGeomDeg; o >= 0; --o) {
+    ny = fma(ny, y, n);
+    n = fma(n, y, A[o]);
+    nx = fma(nx, y, A[5 + o]);
   }
+  N = n;
+  Ns = v_moves ? nx : ny;
+  Nt = v_moves ? ny : nx;
+}
+// rational quotient of the homogeneous jet (splines.cpp:183-216)
+__device__ __forceinline__ void jet_quot(const double N[4], const double Ns[4], const double Nt[4], double x[3],
+                                         double du[3], double dv[3]) {
   const double iw = 1.0 / N[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -376,6 +391,53 @@ __device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_mo
     du[k] = (Ns[k] - x[k] * Ns[3]) * iw;
     dv[k] = (Nt[k] - x[k] * Nt[3]) * iw;
   }
+}
+// Point of a line from its setup at the moving coordinate y.
+__device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_moves, double y, double x[3],
+                                         double du[3], double dv[3]) {
+  double N[4], Ns[4], Nt[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+#if IGB_SING_VEC
+    // 16 B shared loads (st is 16 B aligned): half the load instructions
+    double A[10];
+    const double2* A2 = reinterpret_cast<const double2*>(st + c * 10);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const double2 v = A2[k];
+      A[2 * k] = v.x;
+      A[2 * k + 1] = v.y;
+    }
+#else
+    const double* A = st + c * 10;
+#endif
+    jet_comp(A, v_moves, y, N[c], Ns[c], Nt[c]);
+  }
+  jet_quot(N, Ns, Nt, x, du, dv);
+}
+#ifndef IGB_VERTEX_FIXED
+#define IGB_VERTEX_FIXED 1
+#endif
+// Vertex lines fix both parameters of element a: its setup tasks finish the
+// component's jet at the fixed point ([N, Ns, Nt, -] per component) and the
+// points only form the quotient.
+__device__ __forceinline__ void jet_fixed(const double* __restrict__ st, double x[3], double du[3], double dv[3]) {
+  double N[4], Ns[4], Nt[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+#if IGB_SING_VEC
+    const double2* A2 = reinterpret_cast<const double2*>(st + c * 10);
+    const double2 a = A2[0], b = A2[1];
+    N[c] = a.x;
+    Ns[c] = a.y;
+    Nt[c] = b.x;
+#else
+    N[c] = st[c * 10];
+    Ns[c] = st[c * 10 + 1];
+    Nt[c] = st[c * 10 + 2];
+#endif
+  }
+  jet_quot(N, Ns, Nt, x, du, dv);
 }
 
 // Exact small-integer division by the (runtime) rule order n: float
@@ -488,7 +550,7 @@ struct SingLayout {
   static constexpr int HEAD = 104 * 2 + 2 * KT::TABN + 128;
   static constexpr int STAGE = CH * STR * (SW + 1);
   static constexpr int RED = SL * NL * NL * SW;
-  static constexpr int BODY = STAGE > RED ? STAGE : RED;
+  static constexpr int BODY = ((STAGE > RED ? STAGE : RED) + 1) & ~1;  // keeps the setup lines 16 B aligned
 #ifndef IGB_SING_LMAX
 #define IGB_SING_LMAX 16  // 8 setup tasks per line: one round of 128 threads
 #endif
@@ -514,7 +576,11 @@ struct SingLayout {
   // per line: [element][component][A0..4, B0..4] (80), the affine rule
   // descriptor (c0, c1) x 4 + weight (9); odd stride (the lines of one warp
   // read distinct banks)
+#if IGB_SING_VEC
+  static constexpr int LSTRIDE = 2 * 4 * 10 + 10;  // even: 16 B aligned lines (20-bank offset per line)
+#else
   static constexpr int LSTRIDE = 2 * 4 * 10 + 9;
+#endif
   static constexpr int SETUP = LMAX * LSTRIDE;
   static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY + SETUP) * 8;
   static_assert(NL % TS == 0, "tile");
@@ -591,7 +657,20 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   // (disjoint shared regions), two barriers per chunk
   auto do_setup = [&](int lb) {
     for (int task = tid; task < lpc * 8; task += 128) {
-      const int ll = task >> 3, e = (task >> 2) & 1, c = task & 3;
+      // vertex: element-major task order (e warp-uniform when 4 lpc is a multiple
+      // of 32: the two elements' tasks differ); else line-major (fewer bank
+      // conflicts on the setup stores)
+      int e, ll, c;
+      if (IGB_VERTEX_FIXED && CLS == 1) {
+        e = task >= lpc * 4;
+        const int rem = task - e * lpc * 4;
+        ll = rem >> 2;
+        c = rem & 3;
+      } else {
+        ll = task >> 3;
+        e = (task >> 2) & 1;
+        c = task & 3;
+      }
       const int line = lb + ll;
       if (line < nlines) {
         double c0[4], c1[4], wl;
@@ -601,12 +680,25 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
         const double sx0 = e ? sxb : sxa, sy0 = e ? syb : sya;
         const double f = vm ? sx0 + h * c0[2 * e] : sy0 + h * c0[2 * e + 1];
         double* L = setup + ll * LY::LSTRIDE;
-        jet_setup((e ? cfb : cfa) + c * 25, vm, f, L + (e * 4 + c) * 10);
-        if (task % 8 == 0) {
+        if (IGB_VERTEX_FIXED && CLS == 1 && e == 0) {  // vertex: element a fixed along the line
+          double res[10], N, Ns, Nt;
+          jet_setup_regs(cfa + c * 25, vm, f, res);
+          jet_comp(res, vm, vm ? sya + h * c0[1] : sxa + h * c0[0], N, Ns, Nt);
+          L[c * 10] = N;
+          L[c * 10 + 1] = Ns;
+          L[c * 10 + 2] = Nt;
+        } else {
+          jet_setup((e ? cfb : cfa) + c * 25, vm, f, L + (e * 4 + c) * 10);
+        }
+        if (e == 0 && c == 0) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
+#if IGB_SING_VEC
+            reinterpret_cast<double2*>(L + 80)[k] = make_double2(c0[k], c1[k]);
+#else
             L[80 + 2 * k] = c0[k];
             L[81 + 2 * k] = c1[k];
+#endif
           }
           L[88] = wl;
         }
@@ -623,13 +715,24 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
       if (p < npts) {
         const double* L = setup + my_ll * LY::LSTRIDE;
         const double gk4 = gx[my_k];
+#if IGB_SING_VEC
+        const double2* D = reinterpret_cast<const double2*>(L + 80);
+        const double2 du_ = D[0], dv_ = D[1], dub_ = D[2], dvb_ = D[3];
+        const double ua = fma(du_.y, gk4, du_.x), va = fma(dv_.y, gk4, dv_.x);
+        const double ub = fma(dub_.y, gk4, dub_.x), vb = fma(dvb_.y, gk4, dvb_.x);
+        const int vma = dv_.y != 0.0, vmb = dvb_.y != 0.0;
+#else
         const double ua = fma(L[81], gk4, L[80]), va = fma(L[83], gk4, L[82]);
         const double ub = fma(L[85], gk4, L[84]), vb = fma(L[87], gk4, L[86]);
-        const double w = L[88] * gw[my_k];
         const int vma = L[83] != 0.0, vmb = L[87] != 0.0;
+#endif
+        const double w = L[88] * gw[my_k];
         const double sa_ = sxa + h * ua, ta_ = sya + h * va, sb_ = sxb + h * ub, tb_ = syb + h * vb;
         double xa[3], dua[3], dva[3], xb[3], dub[3], dvb[3];
-        jet_line(L, vma, vma ? ta_ : sa_, xa, dua, dva);
+        if constexpr (IGB_VERTEX_FIXED && CLS == 1)
+          jet_fixed(L, xa, dua, dva);
+        else
+          jet_line(L, vma, vma ? ta_ : sa_, xa, dua, dva);
         jet_line(L + 40, vmb, vmb ? tb_ : sb_, xb, dub, dvb);
         const double sga = sqrt_g_of(dua, dva), sgb = sqrt_g_of(dub, dvb);
         const double d0 = xa[0] - xb[0], d1 = xa[1] - xb[1], d2 = xa[2] - xb[2];
