@@ -148,6 +148,52 @@ __device__ __forceinline__ cd green_c(double r2, const KParams& kp) {
   if (kp.ki != 0.0) a *= exp(kp.ki * r);
   return mk(a * c, -a * s);
 }
+// sin and cos for the far field: x - k pi/2 by two FMAs with a two-part pi/2
+// (k = rint(2x/pi)), then the fdlibm kernel polynomials on [-pi/4, pi/4]
+// (__kernel_sin / __kernel_cos coefficients, error < 2^-58 there) and the
+// quadrant swap; libdevice sincos beyond |x| = 1e5
+__device__ __forceinline__ void sincos_far(double x, double* sn, double* cs) {
+  if (fabs(x) > 1e5) {
+    sincos(x, sn, cs);
+    return;
+  }
+  const double k = rint(x * 0.63661977236758134308);
+  const double y = fma(-k, 6.12323399573676603587e-17, fma(-k, 1.57079632679489655800e+00, x));
+  const double z = y * y;
+  const double ps = fma(fma(fma(fma(fma(1.58969099521155010221e-10, z, -2.50507602534068634195e-08), z,
+                                    2.75573137070700676789e-06), z, -1.98412698298579493134e-04), z,
+                            8.33333333332248946124e-03), z, -1.66666666666666324348e-01);
+  const double pc = fma(fma(fma(fma(fma(-1.13596475577881948265e-11, z, 2.08757232129817482790e-09), z,
+                                    -2.75573143513906633035e-07), z, 2.48015872894767294178e-05), z,
+                            -1.38888888888741095749e-03), z, 4.16666666666666019037e-02);
+  const double s0 = fma(y * z, ps, y);
+  const double c0 = fma(z * z, pc, fma(-0.5, z, 1.0));
+  const int q = __double2int_rn(k);
+  double s = (q & 1) ? c0 : s0, c = (q & 1) ? s0 : c0;
+  if (q & 2) s = -s;
+  if ((q + 1) & 2) c = -c;
+  *sn = s;
+  *cs = c;
+}
+// Green's function for the far field (admissible pairs, r > 0).  Laplace: 1/r
+// from the MUFU estimate and one Newton step (relative error ~1e-13, far below
+// the interpolation error).  Complex kinds: the cubic refinement (~1 ulp: the
+// phase kappa r amplifies an error in r) and the reduced-range sincos above.
+template <class KT>
+__device__ __forceinline__ typename KT::S green_far(double r2, const KParams& kp) {
+  if constexpr (KT::KIND == 0) {
+    double y0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+    return (0.5 * kInv4Pi) * (y0 * fma(-r2 * y0, y0, 3.0));
+  } else {
+    const double ir = rsqrt_nr(r2), r = r2 * ir;
+    double s, c;
+    sincos_far(kp.kr * r, &s, &c);
+    double a = kInv4Pi * ir;
+    if (kp.ki != 0.0) a *= exp(kp.ki * r);
+    return mk(a * c, -a * s);
+  }
+}
 template <class KT>
 __device__ __forceinline__ typename KT::S green_k(double r2, const KParams& kp) {
   if constexpr (KT::KIND == 0)
@@ -155,6 +201,9 @@ __device__ __forceinline__ typename KT::S green_k(double r2, const KParams& kp) 
   else
     return green_c(r2, kp);
 }
+#ifndef IGB_GREEN_FAR
+#define IGB_GREEN_FAR green_far  // A/B: -DIGB_GREEN_FAR=green_k
+#endif
 
 // -------------------------------------------------------- geometry jet
 // cf: [c][j][i] (stride 5 / 25), homogeneous (wx, wy, wz, w) in (s, t)

@@ -1086,7 +1086,7 @@ __global__ void __launch_bounds__(256) k_far_fused(int n_targets, const int* __r
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const double d0 = tx[r][0] - xy.x, d1 = tx[r][1] - xy.y, d2 = tx[r][2] - sz;
-          const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+          const S gk = IGB_GREEN_FAR<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
 #pragma unroll
           for (int c = 0; c < NCH; ++c) fmac(part[c][r], gk, xv[c]);
         }
@@ -1203,7 +1203,7 @@ __global__ void __launch_bounds__(256) k_far_sym_w(int n_targets, const int* __r
       for (int r = 0; r < R; ++r) {
         if (lane + 32 * r >= mm) continue;
         const double d0 = tx[r][0] - xy.x, d1 = tx[r][1] - xy.y, d2 = tx[r][2] - sz;
-        const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+        const S gk = IGB_GREEN_FAR<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           fmac(acc[c][r], gk, xs[c]);
