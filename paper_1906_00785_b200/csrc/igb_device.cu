@@ -418,6 +418,9 @@ __device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_mo
 #ifndef IGB_VERTEX_FIXED
 #define IGB_VERTEX_FIXED 1
 #endif
+#ifndef IGB_EDGE_I3
+#define IGB_EDGE_I3 1
+#endif
 // Vertex lines fix both parameters of element a: its setup tasks finish the
 // component's jet at the fixed point ([N, Ns, Nt, -] per component) and the
 // points only form the quotient.
@@ -493,6 +496,35 @@ __device__ __forceinline__ void rule_line(int line, int n, float rn, const doubl
   } else if constexpr (CLS == 2) {  // edge (quadrature.cpp:113-149)
     const int kind = sec >> 1;
     const double sgn = (sec & 1) ? -1.0 : 1.0;
+#if IGB_EDGE_I3
+    // lines run over i3 (the decoded innermost index is i4): the element whose
+    // point does not depend on i3 (a for kinds 0 and 2, b for kind 1) is fixed
+    // along the line, the other moves its v (t * gx[i3])
+    const double t = gx[i1], a = gx[i2], g4 = gx[i3];
+    double d, jac;
+    if (kind == 2) {
+      d = sgn * t;
+      jac = t * t * (1.0 - t);
+    } else {
+      d = sgn * t * a;
+      jac = t * t * (1.0 - t * a);
+    }
+    const double u0 = fmax(0.0, -d), ul = 1.0 - fabs(d);
+    c0[0] = fma(ul, g4, u0);     c1[0] = 0.0;
+    c0[2] = fma(ul, g4, u0 + d); c1[2] = 0.0;
+    if (kind == 0) {
+      c0[1] = t;     c1[1] = 0.0;
+      c0[3] = 0.0;   c1[3] = t;
+    } else if (kind == 1) {
+      c0[1] = 0.0;   c1[1] = t;
+      c0[3] = t;     c1[3] = 0.0;
+    } else {
+      c0[1] = t * a; c1[1] = 0.0;
+      c0[3] = 0.0;   c1[3] = t;
+    }
+    wl = w3 * jac;
+    (void)i1;
+#else
     const double t = gx[i1], a = gx[i2], b = gx[i3];
     double d, jac, va, vb;
     if (kind == 0) {
@@ -508,6 +540,7 @@ __device__ __forceinline__ void rule_line(int line, int n, float rn, const doubl
     c0[2] = u0 + d; c1[2] = ul;
     c0[3] = vb;     c1[3] = 0.0;
     wl = w3 * jac;
+#endif
   } else {  // vertex (quadrature.cpp:151-177)
     const double t = gx[i1];
     const double v1 = t * gx[i2], v2 = t * gx[i3];
@@ -634,6 +667,8 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   // under exchanging the two points, so half the sectors give C and the block
   // is C + C^T (the Galerkin symmetry the reference tests, test_assembly.cpp:20-29)
   const bool half = CLS == 3 && ma == mb;
+  // an element fixed along every rule line: vertex (a), edge with lines over i3
+  constexpr bool kFixedEl = (IGB_VERTEX_FIXED && CLS == 1) || (IGB_EDGE_I3 && CLS == 2);
   const int npts = (CLS == 3 ? (half ? 4 : 8) : (CLS == 2 ? 6 : 4)) * n4;
 
   S acc[TS][TS];
@@ -657,11 +692,11 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   // (disjoint shared regions), two barriers per chunk
   auto do_setup = [&](int lb) {
     for (int task = tid; task < lpc * 8; task += 128) {
-      // vertex: element-major task order (e warp-uniform when 4 lpc is a multiple
-      // of 32: the two elements' tasks differ); else line-major (fewer bank
-      // conflicts on the setup stores)
+      // classes with a fixed element (vertex; edge over i3): element-major task
+      // order (e warp-uniform when 4 lpc is a multiple of 32: the two elements'
+      // tasks differ); else line-major (fewer bank conflicts on the setup stores)
       int e, ll, c;
-      if (IGB_VERTEX_FIXED && CLS == 1) {
+      if (kFixedEl) {
         e = task >= lpc * 4;
         const int rem = task - e * lpc * 4;
         ll = rem >> 2;
@@ -680,13 +715,14 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
         const double sx0 = e ? sxb : sxa, sy0 = e ? syb : sya;
         const double f = vm ? sx0 + h * c0[2 * e] : sy0 + h * c0[2 * e + 1];
         double* L = setup + ll * LY::LSTRIDE;
-        if (IGB_VERTEX_FIXED && CLS == 1 && e == 0) {  // vertex: element a fixed along the line
+        if (kFixedEl && (CLS == 1 ? e == 0 : (c1[2 * e] == 0.0 && c1[2 * e + 1] == 0.0))) {  // e fixed on the line
           double res[10], N, Ns, Nt;
-          jet_setup_regs(cfa + c * 25, vm, f, res);
-          jet_comp(res, vm, vm ? sya + h * c0[1] : sxa + h * c0[0], N, Ns, Nt);
-          L[c * 10] = N;
-          L[c * 10 + 1] = Ns;
-          L[c * 10 + 2] = Nt;
+          jet_setup_regs((e ? cfb : cfa) + c * 25, vm, f, res);
+          jet_comp(res, vm, vm ? sy0 + h * c0[2 * e + 1] : sx0 + h * c0[2 * e], N, Ns, Nt);
+          double* Le = L + (e * 4 + c) * 10;
+          Le[0] = N;
+          Le[1] = Ns;
+          Le[2] = Nt;
         } else {
           jet_setup((e ? cfb : cfa) + c * 25, vm, f, L + (e * 4 + c) * 10);
         }
@@ -729,11 +765,27 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
         const double w = L[88] * gw[my_k];
         const double sa_ = sxa + h * ua, ta_ = sya + h * va, sb_ = sxb + h * ub, tb_ = syb + h * vb;
         double xa[3], dua[3], dva[3], xb[3], dub[3], dvb[3];
-        if constexpr (IGB_VERTEX_FIXED && CLS == 1)
-          jet_fixed(L, xa, dua, dva);
-        else
+        if constexpr (kFixedEl) {
+          // vertex: a always fixed, b never; edge: per line (kind 1 fixes b)
+#if IGB_SING_VEC
+          const bool fa = CLS == 1 || (du_.y == 0.0 && dv_.y == 0.0);
+          const bool fbx = CLS != 1 && dub_.y == 0.0 && dvb_.y == 0.0;
+#else
+          const bool fa = CLS == 1 || (L[81] == 0.0 && L[83] == 0.0);
+          const bool fbx = CLS != 1 && L[85] == 0.0 && L[87] == 0.0;
+#endif
+          if (fa)
+            jet_fixed(L, xa, dua, dva);
+          else
+            jet_line(L, vma, vma ? ta_ : sa_, xa, dua, dva);
+          if (fbx)
+            jet_fixed(L + 40, xb, dub, dvb);
+          else
+            jet_line(L + 40, vmb, vmb ? tb_ : sb_, xb, dub, dvb);
+        } else {
           jet_line(L, vma, vma ? ta_ : sa_, xa, dua, dva);
-        jet_line(L + 40, vmb, vmb ? tb_ : sb_, xb, dub, dvb);
+          jet_line(L + 40, vmb, vmb ? tb_ : sb_, xb, dub, dvb);
+        }
         const double sga = sqrt_g_of(dua, dva), sgb = sqrt_g_of(dub, dvb);
         const double d0 = xa[0] - xb[0], d1 = xa[1] - xb[1], d2 = xa[2] - xb[2];
         const S gk = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, g.kp);
