@@ -463,6 +463,13 @@ def main():
         out = out[0]
     if out is not None:
         print(json.dumps(out), flush=True)
+    try:
+        import torch.distributed as tdist
+        if tdist.is_available() and tdist.is_initialized():
+            tdist.barrier()
+            tdist.destroy_process_group()
+    except Exception:  # noqa: BLE001 -- teardown only
+        pass
     return 0
 
 
