@@ -421,6 +421,9 @@ __device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_mo
 #ifndef IGB_EDGE_I3
 #define IGB_EDGE_I3 1
 #endif
+#ifndef IGB_RANK1
+#define IGB_RANK1 1
+#endif
 // Vertex lines fix both parameters of element a: its setup tasks finish the
 // component's jet at the fixed point ([N, Ns, Nt, -] per component) and the
 // points only form the quotient.
@@ -617,6 +620,7 @@ struct SingLayout {
   static constexpr int SETUP = LMAX * LSTRIDE;
   static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY + SETUP) * 8;
   static_assert(NL % TS == 0, "tile");
+  static_assert(CH * STR >= 2 * LMAX * (NL + 1) + 2 * LMAX * NL * SW, "rank-1 buffers fit the staging area");
   static_assert(NT <= 128, "tiles");
 };
 
@@ -669,6 +673,12 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   const bool half = CLS == 3 && ma == mb;
   // an element fixed along every rule line: vertex (a), edge with lines over i3
   constexpr bool kFixedEl = (IGB_VERTEX_FIXED && CLS == 1) || (IGB_EDGE_I3 && CLS == 2);
+  // scalar shapes with a fixed element: the line's contribution is rank one,
+  // s_fixed (x) sum_k gwt_k s_moving,k (or its transpose), so the points stage
+  // gwt s_moving only and the block takes one outer product per line
+  // (measured: P = 4 edge -12 %, vertex -21 %; Helmholtz q = 2 -1..-3 %; real
+  // q = 2 (nl = 9) +2..4 %, where the point-wise GEMM is only ~23 % of the time)
+  constexpr bool kRank1 = kFixedEl && KT::KIND != 2 && NC == 1 && IGB_RANK1 && (NL >= 16 || KT::KIND == 1);
   const int npts = (CLS == 3 ? (half ? 4 : 8) : (CLS == 2 ? 6 : 4)) * n4;
 
   S acc[TS][TS];
@@ -743,7 +753,46 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   };
   do_setup(0);
   __syncthreads();
-  for (int lbase = 0; lbase < nlines; lbase += lpc) {
+  // rank-1 path: s_fixed + orientation [2][LMAX][NL + 1] and line sums
+  // [2][LMAX][NL] double-buffered by chunk, so chunk c's outer products run in
+  // the point phase of chunk c + 1 (two barriers per chunk)
+  double* Fr = Fb;
+  S* Vr = reinterpret_cast<S*>(Fr + 2 * LY::LMAX * (NL + 1));
+  auto gemm1 = [&](int bsel) {
+    if (!active) return;
+    for (int ll = slice; ll < lpc; ll += SL) {
+      const double* f = Fr + (bsel * LY::LMAX + ll) * (NL + 1);
+      const S* v = Vr + (bsel * LY::LMAX + ll) * NL;
+      if (f[NL] != 0.0) {  // a fixed: rows s_fixed, columns the line sum
+        double fr[TS];
+        S vc[TS];
+#pragma unroll
+        for (int i = 0; i < TS; ++i) {
+          fr[i] = f[tr + i];
+          vc[i] = v[tc + i];
+        }
+#pragma unroll
+        for (int i = 0; i < TS; ++i)
+#pragma unroll
+          for (int j = 0; j < TS; ++j) fmac(acc[i][j], vc[j], fr[i]);
+      } else {  // b fixed: rows the line sum, columns s_fixed
+        S vr[TS];
+        double fc[TS];
+#pragma unroll
+        for (int i = 0; i < TS; ++i) {
+          vr[i] = v[tr + i];
+          fc[i] = f[tc + i];
+        }
+#pragma unroll
+        for (int i = 0; i < TS; ++i)
+#pragma unroll
+          for (int j = 0; j < TS; ++j) fmac(acc[i][j], vr[i], fc[j]);
+      }
+    }
+  };
+  (void)gemm1;
+  int rb1 = 0;
+  for (int lbase = 0; lbase < nlines; lbase += lpc, rb1 ^= 1) {
     if (tid < cpts) {
       const int p = lbase * n + tid;
       S* ga = Ga + tid * STR;
@@ -765,15 +814,15 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
         const double w = L[88] * gw[my_k];
         const double sa_ = sxa + h * ua, ta_ = sya + h * va, sb_ = sxb + h * ub, tb_ = syb + h * vb;
         double xa[3], dua[3], dva[3], xb[3], dub[3], dvb[3];
-        if constexpr (kFixedEl) {
-          // vertex: a always fixed, b never; edge: per line (kind 1 fixes b)
+        // vertex: a always fixed, b never; edge: per line (kind 1 fixes b)
 #if IGB_SING_VEC
-          const bool fa = CLS == 1 || (du_.y == 0.0 && dv_.y == 0.0);
-          const bool fbx = CLS != 1 && dub_.y == 0.0 && dvb_.y == 0.0;
+        const bool fa = kFixedEl && (CLS == 1 || (du_.y == 0.0 && dv_.y == 0.0));
+        const bool fbx = kFixedEl && CLS != 1 && dub_.y == 0.0 && dvb_.y == 0.0;
 #else
-          const bool fa = CLS == 1 || (L[81] == 0.0 && L[83] == 0.0);
-          const bool fbx = CLS != 1 && L[85] == 0.0 && L[87] == 0.0;
+        const bool fa = kFixedEl && (CLS == 1 || (L[81] == 0.0 && L[83] == 0.0));
+        const bool fbx = kFixedEl && CLS != 1 && L[85] == 0.0 && L[87] == 0.0;
 #endif
+        if constexpr (kFixedEl) {
           if (fa)
             jet_fixed(L, xa, dua, dva);
           else
@@ -794,28 +843,63 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
         double sa[NC][NL], sb[NC][NL];
         shapes<KT>(taba, ua, va, h, dua, dva, sga, sa);
         shapes<KT>(tabb, ub, vb, h, dub, dvb, sgb, sb);
+        if constexpr (kRank1) {
+          // ga holds gwt s_moving; the line's first point stores s_fixed + orientation
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          S wc = gwt;
-          if constexpr (KT::KIND == 2) {
-            if (c == 3) wc = gwt * mk(g.kp.dwx, g.kp.dwy);
+          for (int l = 0; l < NL; ++l) ga[l] = gwt * (fa ? sb[0][l] : sa[0][l]);
+          if (my_k == 0) {
+            double* f = Fr + (rb1 * LY::LMAX + my_ll) * (NL + 1);
+#pragma unroll
+            for (int l = 0; l < NL; ++l) f[l] = fa ? sa[0][l] : sb[0][l];
+            f[NL] = fa ? 1.0 : 0.0;
           }
+        } else {
+          (void)fbx;
 #pragma unroll
-          for (int l = 0; l < NL; ++l) {
-            ga[c * NL + l] = wc * sa[c][l];
-            fb[c * NL + l] = sb[c][l];
+          for (int c = 0; c < NC; ++c) {
+            S wc = gwt;
+            if constexpr (KT::KIND == 2) {
+              if (c == 3) wc = gwt * mk(g.kp.dwx, g.kp.dwy);
+            }
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+              ga[c * NL + l] = wc * sa[c][l];
+              fb[c * NL + l] = sb[c][l];
+            }
           }
         }
       } else {
+        if constexpr (kRank1) {
 #pragma unroll
-        for (int c = 0; c < NC * NL; ++c) {
-          ga[c] = zero<S>();
-          fb[c] = 0.0;
+          for (int l = 0; l < NL; ++l) ga[l] = zero<S>();
+          if (my_k == 0) {
+            double* f = Fr + (rb1 * LY::LMAX + my_ll) * (NL + 1);
+#pragma unroll
+            for (int l = 0; l <= NL; ++l) f[l] = 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC * NL; ++c) {
+            ga[c] = zero<S>();
+            fb[c] = 0.0;
+          }
         }
       }
     }
+    if constexpr (kRank1) {
+      if (lbase > 0) gemm1(rb1 ^ 1);
+    }
     __syncthreads();
-    if (active) {
+    if constexpr (kRank1) {
+      // line sums V[ll][l] = sum_k gwt_k s_moving,k[l] (fixed order)
+      for (int task = tid; task < lpc * NL; task += 128) {
+        const int ll = task / NL, l = task - ll * NL;
+        const S* m = Ga + ll * n * STR + l;
+        S sum = zero<S>();
+        for (int k = 0; k < n; ++k) sum = sum + m[k * STR];
+        Vr[(rb1 * LY::LMAX + ll) * NL + l] = sum;
+      }
+    } else if (active) {
       for (int pt = slice; pt < cpts; pt += SL) {
         const S* ga = Ga + pt * STR;
         const double* fb = Fb + pt * STR;
@@ -836,6 +920,10 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
       }
     }
     if (lbase + lpc < nlines) do_setup(lbase + lpc);
+    __syncthreads();
+  }
+  if constexpr (kRank1) {
+    gemm1(rb1 ^ 1);
     __syncthreads();
   }
   S* red = reinterpret_cast<S*>(body);
