@@ -1383,6 +1383,9 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static constexpr int MM = M * M;
   // m = 4: 4 x 8 lanes (A/B on B200: 0.37 ms vs 0.41 ms for 2 x 16 at c2);
   // m = 5: 5 x 6 lanes, an exact 5 x 5 tile each (30 of 32 lanes)
+#ifndef IGB_FAR_IDX_AHEAD
+#define IGB_FAR_IDX_AHEAD 1
+#endif
 #ifndef IGB_M4_MINB
 #define IGB_M4_MINB 3
 #endif
@@ -1454,8 +1457,18 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
   // (evaluated by s's warp).  Single GPU: every s owned, only s > t visited.
   const int q0 = (DIST && full_row) ? far_rs[t] : upper_start[t], q1 = far_rs[t + 1];
   double nsx[CN][3], nxs[CN];
+  // single GPU: source indices read one pair ahead, so the image loads of pair
+  // q depend on a register, not on a load issued in the same iteration
+  constexpr bool kAhead = IGB_FAR_IDX_AHEAD && !DIST;
+  int s_nx = (kAhead && q0 < q1) ? __ldg(far_b + q0) : 0;
   auto load = [&](int q) {
-    const int s = far_b[q];
+    int s;
+    if constexpr (kAhead) {
+      s = s_nx;
+      if (q + 1 < q1) s_nx = __ldg(far_b + q + 1);
+    } else {
+      s = far_b[q];
+    }
 #pragma unroll
     for (int j = 0; j < CN; ++j) {
       const int mu = bj + BC * j;
