@@ -577,6 +577,9 @@ struct SingArgs {
   double* out;  // compact blocks [item][la][lb] (scattered by k_sing_scatter)
 };
 
+#ifndef IGB_SING_LMAX
+#define IGB_SING_LMAX 16  // 8 setup tasks per line: one round of 128 threads
+#endif
 template <class KT>
 struct SingLayout {
   static constexpr int NL = KT::NL, NC = KT::NC, CH = KT::CHUNK, TS = KT::TS;
@@ -586,10 +589,10 @@ struct SingLayout {
   static constexpr int HEAD = 104 * 2 + 2 * KT::TABN + 128;
   static constexpr int STAGE = CH * STR * (SW + 1);
   static constexpr int RED = SL * NL * NL * SW;
-  static constexpr int BODY = ((STAGE > RED ? STAGE : RED) + 1) & ~1;  // keeps the setup lines 16 B aligned
-#ifndef IGB_SING_LMAX
-#define IGB_SING_LMAX 16  // 8 setup tasks per line: one round of 128 threads
-#endif
+  static constexpr int R1 = CH * STR * SW + 2 * IGB_SING_LMAX * (NL + 1) + 2 * IGB_SING_LMAX * NL * SW;  // rank-1 path
+  static constexpr int BODY0 = STAGE > RED ? STAGE : RED;
+  static constexpr int BODY1 = (KT::KIND != 2 && R1 > BODY0) ? R1 : BODY0;
+  static constexpr int BODY = (BODY1 + 1) & ~1;  // keeps the setup lines 16 B aligned
   static constexpr int LMAX = IGB_SING_LMAX;    // rule lines per chunk (setup capacity)
   // real kernels with up to 9 local functions fit 128 registers: 4 CTAs / SM
 #ifndef IGB_SING_MINB
@@ -620,7 +623,6 @@ struct SingLayout {
   static constexpr int SETUP = LMAX * LSTRIDE;
   static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY + SETUP) * 8;
   static_assert(NL % TS == 0, "tile");
-  static_assert(CH * STR >= 2 * LMAX * (NL + 1) + 2 * LMAX * NL * SW, "rank-1 buffers fit the staging area");
   static_assert(NT <= 128, "tiles");
 };
 
