@@ -580,10 +580,15 @@ struct SingArgs {
 #ifndef IGB_SING_LMAX
 #define IGB_SING_LMAX 16  // 8 setup tasks per line: one round of 128 threads
 #endif
-template <class KT>
+#ifndef IGB_SING_NTH96
+#define IGB_SING_NTH96 1
+#endif
+// NTH threads per CTA: 128, or 96 when a chunk holds <= 96 points (n = 6: 16
+// lines x 6), so no warp idles through the point phase and 5 CTAs fit an SM
+template <class KT, int NTH = 128>
 struct SingLayout {
   static constexpr int NL = KT::NL, NC = KT::NC, CH = KT::CHUNK, TS = KT::TS;
-  static constexpr int NTR = NL / TS, NT = NTR * NTR, SL = 128 / NT;
+  static constexpr int NTR = NL / TS, NT = NTR * NTR, SL = NTH / NT;
   static constexpr int STR = ((NC * NL) % 2 == 0) ? NC * NL + 1 : NC * NL;
   static constexpr int SW = sizeof(typename KT::S) / 8;
   static constexpr int HEAD = 104 * 2 + 2 * KT::TABN + 128;
@@ -607,7 +612,11 @@ struct SingLayout {
 #ifndef IGB_SING_MINBH
 #define IGB_SING_MINBH 4
 #endif
-  static constexpr int MINB = (KT::KIND == 0 && NL <= 9)    ? IGB_SING_MINB
+#ifndef IGB_SING_MINB96
+#define IGB_SING_MINB96 5
+#endif
+  static constexpr int MINB = (NTH == 96)                     ? (NL <= 9 && KT::KIND != 2 ? IGB_SING_MINB96 : 1)
+                              : (KT::KIND == 0 && NL <= 9)    ? IGB_SING_MINB
                               : (KT::KIND == 0 && NL <= 16) ? IGB_SING_MINB16
                               : (KT::KIND == 1 && NL <= 9)  ? IGB_SING_MINBH
                               : (KT::KIND == 2 && NL <= 12) ? IGB_SING_MINBM
@@ -623,13 +632,21 @@ struct SingLayout {
   static constexpr int SETUP = LMAX * LSTRIDE;
   static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY + SETUP) * 8;
   static_assert(NL % TS == 0, "tile");
-  static_assert(NT <= 128, "tiles");
+  static_assert(NT <= NTH, "tiles");
 };
+// the 96-thread variant serves chunks of <= 96 points of Helmholtz kernels with
+// up to 9 local functions (measured: Helmholtz q = 2 edge / vertex -3..-4 %;
+// real q = 2 +1..2 %, so real kernels keep 128 threads)
+template <class KT>
+constexpr bool sing96_ok() {
+  return IGB_SING_NTH96 && KT::KIND == 1 && KT::NL <= 9;
+}
+inline bool sing96_use(int n) { return (IGB_SING_LMAX < 128 / n ? IGB_SING_LMAX : 128 / n) * n <= 96; }
 
-template <class KT, int CLS>
-__global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs g, SingArgs A) {
+template <class KT, int CLS, int NTH = 128>
+__global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(GeoArgs g, SingArgs A) {
   using S = typename KT::S;
-  using LY = SingLayout<KT>;
+  using LY = SingLayout<KT, NTH>;
   constexpr int NL = KT::NL, NC = KT::NC, CH = LY::CH, TS = LY::TS, NTR = LY::NTR, NT = LY::NT,
                 SL = LY::SL, STR = LY::STR;
   extern __shared__ __align__(16) double sm[];
@@ -652,12 +669,12 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   const int n1 = 1 << g.level;
   const int ra = ea % g.epp, rb = eb % g.epp;
   const int ixa = ra % n1, iya = ra / n1, ixb = rb % n1, iyb = rb / n1;
-  for (int i = tid; i < 104; i += 128) {
+  for (int i = tid; i < 104; i += NTH) {
     cfa[i] = g.cells[static_cast<size_t>(cella) * kCellStride + i];
     cfb[i] = g.cells[static_cast<size_t>(cellb) * kCellStride + i];
   }
-  load_tables<KT>(taba, g.tab_a, g.tab_b, ixa, iya, tid, 128);
-  load_tables<KT>(tabb, g.tab_a, g.tab_b, ixb, iyb, tid, 128);
+  load_tables<KT>(taba, g.tab_a, g.tab_b, ixa, iya, tid, NTH);
+  load_tables<KT>(tabb, g.tab_a, g.tab_b, ixb, iyb, tid, NTH);
   const int n = A.n;
   if (tid < n) {
     gx[tid] = A.gx[tid];
@@ -697,13 +714,13 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   // (task (e, c) = (0, 0) also stores the line's affine rule descriptor);
   // then one thread per point finishes both jets from the setup.
   const int nlines = npts / n;
-  const int lpc = min(LY::LMAX, CH / n), cpts = lpc * n;
+  const int lpc = min(LY::LMAX, (CH < NTH ? CH : NTH) / n), cpts = lpc * n;
   const float rn = 1.0f / static_cast<float>(n);
   const int my_ll = div_n(tid, n, rn), my_k = tid - my_ll * n;  // this thread's point of a chunk
   // phases per chunk: point evaluation | GEMM of this chunk + setup of the next
   // (disjoint shared regions), two barriers per chunk
   auto do_setup = [&](int lb) {
-    for (int task = tid; task < lpc * 8; task += 128) {
+    for (int task = tid; task < lpc * 8; task += NTH) {
       // classes with a fixed element (vertex; edge over i3): element-major task
       // order (e warp-uniform when 4 lpc is a multiple of 32: the two elements'
       // tasks differ); else line-major (fewer bank conflicts on the setup stores)
@@ -894,7 +911,7 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
     __syncthreads();
     if constexpr (kRank1) {
       // line sums V[ll][l] = sum_k gwt_k s_moving,k[l] (fixed order)
-      for (int task = tid; task < lpc * NL; task += 128) {
+      for (int task = tid; task < lpc * NL; task += NTH) {
         const int ll = task / NL, l = task - ll * NL;
         const S* m = Ga + ll * n * STR + l;
         S sum = zero<S>();
@@ -937,7 +954,7 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   }
   __syncthreads();
   S* out = reinterpret_cast<S*>(A.out) + static_cast<size_t>(pr) * NL * NL;
-  for (int o = tid; o < NL * NL; o += 128) {
+  for (int o = tid; o < NL * NL; o += NTH) {
     S v = zero<S>();
     for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + o];
     if (half) {
@@ -949,6 +966,25 @@ __global__ void __launch_bounds__(128, SingLayout<KT>::MINB) k_singular(GeoArgs 
   }
 }
 
+}  // namespace dev
+// one launch of a singular class: 96-thread CTAs when the chunk holds <= 96 points
+template <class KT, int CLS>
+void launch_singular(const dev::GeoArgs& g, const dev::SingArgs& A, cudaStream_t st) {
+  if constexpr (dev::sing96_ok<KT>()) {
+    if (dev::sing96_use(A.n)) {
+      using LY = dev::SingLayout<KT, 96>;
+      IGB_CUDA(cudaFuncSetAttribute(dev::k_singular<KT, CLS, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(LY::BYTES)));
+      dev::k_singular<KT, CLS, 96><<<A.n_pairs, 96, LY::BYTES, st>>>(g, A);
+      return;
+    }
+  }
+  using LY = dev::SingLayout<KT, 128>;
+  IGB_CUDA(cudaFuncSetAttribute(dev::k_singular<KT, CLS, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(LY::BYTES)));
+  dev::k_singular<KT, CLS, 128><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
+}
+namespace dev {
 // Singular blocks are integrated before the block partition exists (they only
 // need the mesh topology); once the near list is known each item's block goes
 // to the slot of (ea, eb) and its transpose to the slot of (eb, ea) (the
@@ -2227,7 +2263,6 @@ void H2Device::launch_element_phase(cudaEvent_t* ev, int& launched) {
     IGB_CUDA(cudaGetLastError());
   }
   IGB_CUDA(cudaEventRecord(ev[kEvElements], stream_));
-  using LY = SingLayout<KT>;
   auto launch = [&](auto cls_tag, int evi) {
     constexpr int CLS = decltype(cls_tag)::value;
     const SingList& L = sing_items_[CLS];
@@ -2242,9 +2277,7 @@ void H2Device::launch_element_phase(cudaEvent_t* ev, int& launched) {
       A.gx = as_.gxs;
       A.gw = as_.gws;
       A.out = d_sing_blk_[CLS];
-      IGB_CUDA(cudaFuncSetAttribute(k_singular<KT, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(LY::BYTES)));
-      k_singular<KT, CLS><<<A.n_pairs, 128, LY::BYTES, stream_>>>(g, A);
+      launch_singular<KT, CLS>(g, A, stream_);
       ++launched;
       IGB_CUDA(cudaGetLastError());
     }
@@ -3028,9 +3061,7 @@ static void dense_impl(const Discretization& d, int far_order, int sing_order, i
         A.gx = d_gxs;
         A.gw = d_gws;
         A.out = reinterpret_cast<double*>(d_sblk[CLS]);
-        IGB_CUDA(cudaFuncSetAttribute(k_singular<KT, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(LY::BYTES)));
-        k_singular<KT, CLS><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
+        launch_singular<KT, CLS>(g, A, st);
         IGB_CUDA(cudaGetLastError());
       };
       launch(std::integral_constant<int, 3>{});
