@@ -1421,6 +1421,9 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static constexpr int MM = M * M;
   // m = 4: 4 x 8 lanes (A/B on B200: 0.37 ms vs 0.41 ms for 2 x 16 at c2);
   // m = 5: 5 x 6 lanes, an exact 5 x 5 tile each (30 of 32 lanes)
+#ifndef IGB_FUSED_NEAR
+#define IGB_FUSED_NEAR 1  // single GPU, m = 4: leaf far field and near rows in one kernel
+#endif
 #ifndef IGB_FAR_IDX_AHEAD
 #define IGB_FAR_IDX_AHEAD 1
 #endif
@@ -1463,13 +1466,13 @@ constexpr double kFarScale = kInv4Pi;
 // gives down[t] += K up[s] (accumulated in registers) and K^T up[t], written to
 // the slot of the transposed pair (s, t) and summed by k_far_lower in fixed
 // order.  Lane (bi, bj) owns RN target rows x CN source columns.
-template <int M, bool DIST, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int* __restrict__ targets,
-                                                 const int* __restrict__ upper_start, const int* __restrict__ far_rs,
-                                                 const int* __restrict__ far_b, const int* __restrict__ trans,
-                                                 const double* __restrict__ img, const double* __restrict__ up,
-                                                 double* __restrict__ down, double* __restrict__ slot,
-                                                 const unsigned char* __restrict__ owned, int full_row) {
+template <int M, bool DIST>
+__device__ __forceinline__ void far_sym_body(int n_targets, const int* __restrict__ targets,
+                                             const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+                                             const int* __restrict__ far_b, const int* __restrict__ trans,
+                                             const double* __restrict__ img, const double* __restrict__ up,
+                                             double* __restrict__ down, double* __restrict__ slot,
+                                             const unsigned char* __restrict__ owned, int full_row) {
   using T = SymTile<M>;
   constexpr int MM = T::MM, BR = T::BR, BC = T::BC, RN = T::RN, CN = T::CN;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1586,6 +1589,15 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
   }
 }
 
+template <int M, bool DIST, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int* __restrict__ targets,
+                                                 const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+                                                 const int* __restrict__ far_b, const int* __restrict__ trans,
+                                                 const double* __restrict__ img, const double* __restrict__ up,
+                                                 double* __restrict__ down, double* __restrict__ slot,
+                                                 const unsigned char* __restrict__ owned, int full_row) {
+  far_sym_body<M, DIST>(n_targets, targets, upper_start, far_rs, far_b, trans, img, up, down, slot, owned, full_row);
+}
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
 // in ascending t (fixed order)
 // Unconditional, unrolled stream over the row's contiguous slots.  Multi-GPU:
@@ -1665,19 +1677,15 @@ __global__ void k_unpack(int n, const int* __restrict__ nodes, int rows, const S
 // near-field rows per test element (h2.cpp:349-357); one warp per element,
 // streaming its contiguous row [la][k][lb]
 // FROM_X: coefficients gathered inline from x (l2g, signs) instead of coef
-template <class S, int NL, bool FROM_X = false>
-__global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict__ near_rs,
-                                                   const int* __restrict__ near_b, const S* __restrict__ blk,
-                                                   const S* __restrict__ coef, S* __restrict__ rows_out,
-                                                   const int* __restrict__ l2g = nullptr,
-                                                   const double* __restrict__ sg = nullptr) {
+template <class S, int NL, bool FROM_X>
+__device__ __forceinline__ void near_row(int e, int lane, const int* __restrict__ near_rs,
+                                         const int* __restrict__ near_b, const S* __restrict__ blk,
+                                         const S* __restrict__ coef, S* __restrict__ rows_out,
+                                         const int* __restrict__ l2g, const double* __restrict__ sg) {
   auto cf = [&](int k) -> S {
     if constexpr (FROM_X) return coef[l2g[k]] * sg[k];
     else return coef[k];
   };
-  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (e >= ne) return;
   const int rs = near_rs[e], cnt = near_rs[e + 1] - rs;
   const int len = cnt * NL;
   const S* base = blk + static_cast<size_t>(rs) * NL * NL;
@@ -1709,6 +1717,45 @@ __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict
     const S a = warp_sum(acc[l]);
     if (lane == 0) rows_out[static_cast<size_t>(e) * NL + l] = a;
   }
+}
+template <class S, int NL, bool FROM_X = false>
+__global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict__ near_rs,
+                                                   const int* __restrict__ near_b, const S* __restrict__ blk,
+                                                   const S* __restrict__ coef, S* __restrict__ rows_out,
+                                                   const int* __restrict__ l2g = nullptr,
+                                                   const double* __restrict__ sg = nullptr) {
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (e >= ne) return;
+  near_row<S, NL, FROM_X>(e, threadIdx.x & 31, near_rs, near_b, blk, coef, rows_out, l2g, sg);
+}
+
+// Leaf-level far field fused with the near rows (single GPU): warp w < n_fine
+// evaluates leaf target fine[w]'s far pairs, then streams the near row of that
+// leaf's element; the remaining warps stream the rows of elements without leaf
+// far pairs.  The HBM-bound rows thus run at the tail of each warp while other
+// warps of the SM are still in the FP64-bound far loop (the separate near-row
+// kernel could not share SMs with the far field).
+template <int M, int NL, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_far_sym_near(
+    int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
+    int leaf_off, const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+    const int* __restrict__ far_b, const int* __restrict__ trans, const double* __restrict__ img,
+    const double* __restrict__ up, double* __restrict__ down, double* __restrict__ slot,
+    const unsigned char* __restrict__ owned, const int* __restrict__ near_rs, const int* __restrict__ near_b,
+    const double* __restrict__ blk, const double* __restrict__ x, double* __restrict__ rows_out,
+    const int* __restrict__ l2g, const double* __restrict__ sg) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int e;
+  if (warp < n_fine) {
+    far_sym_body<M, false>(n_fine, fine, upper_start, far_rs, far_b, trans, img, up, down, slot, owned, 0);
+    const int t = fine[warp];
+    e = (t / npp) * epp + (t % npp - leaf_off);
+  } else if (warp < n_fine + n_rest) {
+    e = rest[warp - n_fine];
+  } else {
+    return;
+  }
+  near_row<double, NL, true>(e, threadIdx.x & 31, near_rs, near_b, blk, x, rows_out, l2g, sg);
 }
 
 // leaf backward transform moments^T down + near rows (h2.cpp:359-371); one
@@ -2198,6 +2245,20 @@ void H2Device::stage_plan() {
       n_sym_coarse_ = static_cast<int>(coarse.size());
       d_sym_fine_ = upload(fine);
       d_sym_coarse_ = upload(coarse);
+      // fused leaf far field + near rows (single GPU, m = 4): the elements whose
+      // leaf has no upper far pairs get near-only warps
+      bool ident = Lp.world == 1 && static_cast<int>(Lp.el.size()) == d.element_count();
+      for (size_t i = 0; ident && i < Lp.el.size(); ++i) ident = Lp.el[i] == static_cast<int>(i);
+      if (IGB_FUSED_NEAR && sym_far_ && m == 4 && ident) {
+        std::vector<char> has(d.element_count(), 0);
+        const int epp = d.elements_per_patch();
+        for (int t : fine) has[(t / P.npp) * epp + (t % P.npp - P.level_offset[P.depth])] = 1;
+        std::vector<int> rest;
+        for (int e = 0; e < d.element_count(); ++e)
+          if (!has[e]) rest.push_back(e);
+        n_near_rest_ = static_cast<int>(rest.size());
+        d_near_rest_ = upload(rest);
+      }
       d_upper_start_ = upload(P.far_upper_start);
       d_trans_ = upload(P.far_trans);
       const size_t per_pair = static_cast<size_t>(mm) * (sym_w_ ? static_cast<size_t>(nch_) * sw : 1);
@@ -2635,11 +2696,14 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   int launches = 0;
   (void)nloc;
   (void)coef;
+  const bool fused = KT::KIND == 0 && NL <= 16 && n_near_rest_ >= 0;
   IGB_CUDA(cudaEventRecord(ev_fork_, s));
   IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-  k_near_rows<S, NL, true><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
-      nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), x, nrows, d_l2g_, d_lsign_);
-  ++launches;
+  if (!fused) {
+    k_near_rows<S, NL, true><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
+        nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), x, nrows, d_l2g_, d_lsign_);
+    ++launches;
+  }
   IGB_CUDA(cudaEventRecord(ev_join_, side_));
   const long long ndown = static_cast<long long>(P.n_nodes) * rows;
   pdl_launch(k_leaf_up_x<S, NL>, grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s, 
@@ -2680,8 +2744,20 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
     ++launches;
   }
   IGB_CUDA(cudaEventRecord(ev_join2_, side2_));
-  // main: leaf-level far field
-  far_sym(s, n_sym_fine_, d_sym_fine_);
+  // main: leaf-level far field (fused with the near rows when enabled)
+  if (fused) {
+    if constexpr (KT::KIND == 0 && NL <= 16) {
+      const long long nw = static_cast<long long>(n_sym_fine_) + n_near_rest_;
+      k_far_sym_near<4, NL, IGB_M4_MINB><<<grid_for(nw * 32, 256), 256, 0, s>>>(
+          n_sym_fine_, d_sym_fine_, n_near_rest_, d_near_rest_, epp, npp, P.level_offset[L], d_upper_start_,
+          d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, d_near_rs_, d_near_b_,
+          reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
+          reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
+      ++launches;
+    }
+  } else {
+    far_sym(s, n_sym_fine_, d_sym_fine_);
+  }
   far_lower(s, 1);
   IGB_CUDA(cudaStreamWaitEvent(s, ev_join2_, 0));
   {

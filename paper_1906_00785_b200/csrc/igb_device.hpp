@@ -140,6 +140,8 @@ class H2Device {
   int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;
   int n_sym_fine_ = 0, n_sym_coarse_ = 0;  // leaf-level / coarser symmetric targets
   int *d_sym_fine_ = nullptr, *d_sym_coarse_ = nullptr;
+  int n_near_rest_ = -1;  // fused leaf far field + near rows: elements without leaf targets (-1: off)
+  int* d_near_rest_ = nullptr;
   double* d_slot_ = nullptr;
   int *d_far_a_ = nullptr;
   int *d_dof_start_ = nullptr, *d_dof_inc_ = nullptr;
