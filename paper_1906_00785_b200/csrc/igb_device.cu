@@ -2249,7 +2249,7 @@ void H2Device::stage_plan() {
       // leaf has no upper far pairs get near-only warps
       bool ident = Lp.world == 1 && static_cast<int>(Lp.el.size()) == d.element_count();
       for (size_t i = 0; ident && i < Lp.el.size(); ++i) ident = Lp.el[i] == static_cast<int>(i);
-      if (IGB_FUSED_NEAR && sym_far_ && m == 4 && ident) {
+      if (IGB_FUSED_NEAR && sym_far_ && (m == 4 || m == 5) && ident) {
         std::vector<char> has(d.element_count(), 0);
         const int epp = d.elements_per_patch();
         for (int t : fine) has[(t / P.npp) * epp + (t % P.npp - P.level_offset[P.depth])] = 1;
@@ -2748,11 +2748,17 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   if (fused) {
     if constexpr (KT::KIND == 0 && NL <= 16) {
       const long long nw = static_cast<long long>(n_sym_fine_) + n_near_rest_;
-      k_far_sym_near<4, NL, IGB_M4_MINB><<<grid_for(nw * 32, 256), 256, 0, s>>>(
-          n_sym_fine_, d_sym_fine_, n_near_rest_, d_near_rest_, epp, npp, P.level_offset[L], d_upper_start_,
-          d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, d_near_rs_, d_near_b_,
-          reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
-          reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
+      auto fused_launch = [&](auto kern) {
+        kern<<<grid_for(nw * 32, 256), 256, 0, s>>>(
+            n_sym_fine_, d_sym_fine_, n_near_rest_, d_near_rest_, epp, npp, P.level_offset[L], d_upper_start_,
+            d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, d_near_rs_, d_near_b_,
+            reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
+            reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
+      };
+      if (m == 4)
+        fused_launch(k_far_sym_near<4, NL, IGB_M4_MINB>);
+      else
+        fused_launch(k_far_sym_near<5, NL, IGB_M5_MINB>);
       ++launches;
     }
   } else {
