@@ -1421,6 +1421,9 @@ struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
   static constexpr int MM = M * M;
   // m = 4: 4 x 8 lanes (A/B on B200: 0.37 ms vs 0.41 ms for 2 x 16 at c2);
   // m = 5: 5 x 6 lanes, an exact 5 x 5 tile each (30 of 32 lanes)
+#ifndef IGB_LEAF_DOWN_V2
+#define IGB_LEAF_DOWN_V2 1
+#endif
 #ifndef IGB_FUSED_NEAR
 #define IGB_FUSED_NEAR 1  // single GPU, m = 4: leaf far field and near rows in one kernel
 #endif
@@ -1774,6 +1777,21 @@ __global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restri
   const S* dn = down + static_cast<size_t>(leaf) * rows;
   const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
   S acc = zero<S>();
+  if constexpr (sizeof(S) == 8 && IGB_LEAF_DOWN_V2) {
+    // rows even (m^2 nch with m even or nch = 4) and 16 B aligned: paired loads
+    if ((rows & 1) == 0) {
+      const double2* m2 = reinterpret_cast<const double2*>(mc);
+      const double2* d2 = reinterpret_cast<const double2*>(dn);
+#pragma unroll 8
+      for (int r = 0; r < rows / 2; ++r) {
+        const double2 a = __ldg(m2 + r), b = d2[r];
+        acc = fma(b.x, a.x, acc);
+        acc = fma(b.y, a.y, acc);
+      }
+      loc[idx] = near_rows[idx] + acc;
+      return;
+    }
+  }
 #pragma unroll 8
   for (int r = 0; r < rows; ++r) fmac(acc, dn[r], __ldg(mc + r));
   loc[idx] = near_rows[idx] + acc;
