@@ -285,7 +285,8 @@ def run_b200(args, c, name):
                                    "flops_per_launch": fl, "kernel_evals": evals, "ms": far_ms,
                                    "note": "couplings evaluated on the fly (symmetric: each unordered pair once)"
                                    if sym else "couplings evaluated on the fly"}
-        kt = traffic.get(f"k_far_sym<{c['m']}>")
+        # the profile path times the unfused far kernels (leaf + coarse launches)
+        kt = traffic.get(f"k_far_sym_standalone<{c['m']}>") or traffic.get(f"k_far_sym<{c['m']}>")
         if kt:
             rooflines["matvec_far"]["traffic"] = kt["dram_read_bytes"] + kt["dram_write_bytes"]
     nb = h.device_bytes()["near"]
