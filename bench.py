@@ -207,7 +207,7 @@ def run_b200(args, c, name):
     if world > 1 or args.force_dist:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device(f"cuda:{local}"))
     else:
         dist = None
     dev = local
