@@ -165,6 +165,13 @@ int igb_h2_reassemble(igb_h2* h, double* device_ms, int* launches);
  * [coef gather, leaf moments, upward transfer, zero, far couplings, downward
  * transfer, near rows + leaf backward, DOF scatter] (h2.cpp:271-376) */
 int igb_h2_profile_apply(igb_h2* h, int iters, double phase_ms[8]);
+/* the single-GPU matvec graph's kernels launched one after another, each timed
+ * with CUDA events (ms summed over iters); names[k*32 .. k*32+31] = kernel k's
+ * role ("far_leaf_near", "upward", ...), *n = kernel count (<= max_n) */
+int igb_h2_profile_kernels(igb_h2* h, int iters, int max_n, char* names, double* ms, int* n);
+/* unordered far pairs the symmetric far-field kernels evaluate per matvec:
+ * pairs[0] on the leaf level, pairs[1] above it (0, 0 for other far kernels) */
+int igb_h2_far_work(const igb_h2* h, long long pairs[2]);
 /* `steps` x (device assembly + `matvecs` matvecs) on the handle stream,
  * CUDA-event timed; *total_ms, *assembly_ms (sum of assembly device time) */
 int igb_h2_bench_steps(igb_h2* h, int steps, int matvecs, double* total_ms, double* assembly_ms);
@@ -243,6 +250,11 @@ int igb_dense_assemble(const igb_discretization* d, int far_order, int sing_orde
 int igb_admissible(const double box_a[6], const double box_b[6], double eta);
 int igb_last_error(char* buf, size_t n);
 int igb_version(void);
+/* device memory of destroyed operators stays reserved in a per-device pool for
+ * the next construction (bounded by IGB_POOL_KEEP_MB); this returns it to the
+ * driver (e.g. before handing the device to another allocator).  No reference
+ * counterpart: the reference holds its operator in host memory. */
+int igb_release_device_memory(int device);
 
 #ifdef __cplusplus
 }

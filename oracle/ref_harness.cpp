@@ -208,7 +208,7 @@ int ref_pair_blocks(void* dp, const int* pairs, long long npairs, int far_order,
 #pragma omp parallel for schedule(dynamic, 16)
       for (int e = 0; e < d.element_count(); ++e)
         if (need[e]) caches[e] = detail::make_far_cache<S>(d, e, nfar);
-#pragma omp parallel for schedule(dynamic, 4)
+#pragma omp parallel for schedule(dynamic, 1)
       for (long long q = 0; q < npairs; ++q) {
         const auto b = detail::pair_block<S>(d, caches, pairs[2 * q], pairs[2 * q + 1], nsing);
         std::memcpy(out + static_cast<size_t>(q) * nl * nl * (sizeof(S) / 8), b.data(), sizeof(S) * nl * nl);

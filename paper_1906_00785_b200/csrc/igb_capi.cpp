@@ -407,6 +407,26 @@ int igb_h2_reassemble(igb_h2* h, double* device_ms, int* launches) {
     if (launches) *launches = h->dev->assembly_kernel_launches();
   });
 }
+int igb_h2_profile_kernels(igb_h2* h, int iters, int max_n, char* names, double* ms, int* n) {
+  return guard([&] {
+    need(h, "h2");
+    need(n, "n");
+    const auto k = h->dev->profile_kernels(iters);
+    *n = static_cast<int>(std::min<size_t>(k.size(), static_cast<size_t>(std::max(max_n, 0))));
+    for (int i = 0; i < *n; ++i) {
+      if (names) std::snprintf(names + 32 * i, 32, "%s", k[i].first.c_str());
+      if (ms) ms[i] = k[i].second;
+    }
+  });
+}
+int igb_h2_far_work(const igb_h2* h, long long pairs[2]) {
+  return guard([&] {
+    need(h, "h2");
+    need(pairs, "pairs");
+    pairs[0] = h->dev->sym_pairs(0);
+    pairs[1] = h->dev->sym_pairs(1);
+  });
+}
 int igb_h2_profile_apply(igb_h2* h, int iters, double phase_ms[8]) {
   return guard([&] {
     need(h, "h2");
@@ -605,6 +625,10 @@ int igb_dense_assemble(const igb_discretization* d, int far_order, int sing_orde
     need(out, "out");
     igb::dense_assemble(*d->d, far_order, sing_order, device, out);
   });
+}
+
+int igb_release_device_memory(int device) {
+  return guard([&] { igb::release_device_memory(device); });
 }
 
 int igb_admissible(const double a[6], const double b[6], double eta) {

@@ -1601,6 +1601,119 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym(int n_targets, const int*
                                                  const unsigned char* __restrict__ owned, int full_row) {
   far_sym_body<M, DIST>(n_targets, targets, upper_start, far_rs, far_b, trans, img, up, down, slot, owned, full_row);
 }
+// Column-stream symmetric far field (Laplace, single GPU): warp per target t.
+// The source columns of all upper pairs (t, s), s > t, are streamed 32 at a
+// time -- lane = one interpolation point mu of one pair, so no lane idles
+// whatever m^2 is -- while the target's m^2 rows sit in shared memory and are
+// broadcast.  Distances in shifted dot form: with c = img[t][0],
+// t' = img[t][nu] - c and s' = img[s][mu] - c,
+//   |t - s|^2 = (|t'|^2 + |s'|^2) - 2 t'.s'   (one add + three FMAs),
+// which is accurate because |t'| and |s'| are bounded by a small multiple of
+// |t - s| on admissible pairs; 2/r from the MUFU estimate + one Newton step.
+// Per evaluation 9 FP64 instructions (vs 11 in the lane-tile kernel), and the
+// transposed product K^T up[t] is one lane's own column sum (no shuffles): it
+// goes straight to the slot of the transposed pair (s, t).  K up[s] is
+// accumulated per row in registers and reduced over the warp at the end by a
+// reduce-scatter butterfly (lane l ends with row l).
+template <int MM>
+struct ColRows {
+  static constexpr int R = MM <= 4 ? 4 : MM <= 8 ? 8 : MM <= 16 ? 16 : 32;  // rows padded to a power of two
+  static_assert(MM <= 32, "column-stream far field: m^2 <= 32");
+};
+template <int MM>
+__device__ __forceinline__ void col_reduce_rows(double (&acc)[ColRows<MM>::R], int lane) {
+  constexpr int R = ColRows<MM>::R;
+  // lanes l and l ^ o (o >= R) hold the same row set: plain sums first
+#pragma unroll
+  for (int o = 16; o >= R; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  // reduce-scatter: at half-width H the lanes with bit H set keep the upper half
+#pragma unroll
+  for (int H = R / 2; H >= 1; H >>= 1) {
+    const bool hi = (lane & H) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double send = hi ? acc[i] : acc[i + H];
+      const double keep = hi ? acc[i + H] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+    }
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict__ sh,
+                                             const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+                                             const int* __restrict__ far_b, const int* __restrict__ trans,
+                                             const double* __restrict__ img, const double* __restrict__ up,
+                                             double* __restrict__ down, double* __restrict__ slot) {
+  constexpr int MM = M * M, R = ColRows<MM>::R;
+  // target rows: sh[4 nu .. 4 nu + 3] = (-2 t'x, -2 t'y, -2 t'z, |t'|^2) (two
+  // 16 B broadcasts), sh[4 MM + nu] = up[t][nu]
+  const double* ti = img + static_cast<size_t>(t) * MM * 3;
+  const double cx = __ldg(ti), cy = __ldg(ti + 1), cz = __ldg(ti + 2);
+  for (int nu = lane; nu < MM; nu += 32) {
+    const double x = __ldg(ti + 3 * nu) - cx, y = __ldg(ti + 3 * nu + 1) - cy, z = __ldg(ti + 3 * nu + 2) - cz;
+    double* r = sh + 4 * nu;
+    r[0] = -2.0 * x;
+    r[1] = -2.0 * y;
+    r[2] = -2.0 * z;
+    r[3] = x * x + y * y + z * z;
+    sh[4 * MM + nu] = __ldg(up + static_cast<size_t>(t) * MM + nu);
+  }
+  __syncwarp();
+  double acc[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) acc[i] = 0.0;
+  const int q0 = upper_start[t];
+  const int ncol = (far_rs[t + 1] - q0) * MM;
+  for (int c0 = 0; c0 < ncol; c0 += 32) {
+    const int c = c0 + lane;
+    const bool ok = c < ncol;
+    const int qi = ok ? c / MM : 0, mu = ok ? c - qi * MM : 0;
+    const int q = q0 + qi;
+    const int s = ok ? __ldg(far_b + q) : t;
+    const double* p = img + (static_cast<size_t>(s) * MM + mu) * 3;
+    double sx = __ldg(p) - cx, sy = __ldg(p + 1) - cy, sz = __ldg(p + 2) - cz;
+    double xs = __ldg(up + static_cast<size_t>(s) * MM + mu);
+    if (!ok) {  // padding column: far away (finite kernel), zero weight
+      sx = 1.0e8;
+      sy = sz = 0.0;
+      xs = 0.0;
+    }
+    const double ns = sx * sx + sy * sy + sz * sz;
+    double ps0 = 0.0, ps1 = 0.0;
+#pragma unroll
+    for (int nu = 0; nu < MM; ++nu) {
+      const double2 a01 = *reinterpret_cast<const double2*>(sh + 4 * nu);
+      const double2 a23 = *reinterpret_cast<const double2*>(sh + 4 * nu + 2);
+      const double xt = sh[4 * MM + nu];
+      const double r2 = fma(a01.x, sx, fma(a01.y, sy, fma(a23.x, sz, a23.y + ns)));
+      const double gk = far_rsqrt(r2);  // kFarScale * 4 pi G
+      acc[nu] = fma(gk, xs, acc[nu]);
+      if (nu & 1) ps1 = fma(gk, xt, ps1);
+      else ps0 = fma(gk, xt, ps0);
+    }
+    if (ok) slot[static_cast<size_t>(__ldg(trans + q)) * MM + mu] = (ps0 + ps1) * kFarScale;
+  }
+  col_reduce_rows<MM>(acc, lane);
+  if (lane < MM) down[static_cast<size_t>(t) * MM + lane] = acc[0] * kFarScale;
+}
+
+template <int M, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_far_col(int n_targets, const int* __restrict__ targets,
+                                                      const int* __restrict__ upper_start,
+                                                      const int* __restrict__ far_rs, const int* __restrict__ far_b,
+                                                      const int* __restrict__ trans, const double* __restrict__ img,
+                                                      const double* __restrict__ up, double* __restrict__ down,
+                                                      double* __restrict__ slot) {
+  __shared__ __align__(16) double sh[8][(5 * M * M + 1) / 2 * 2];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= n_targets) return;
+  far_col_body<M>(targets[warp], threadIdx.x & 31, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img,
+                  up, down, slot);
+}
+
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
 // in ascending t (fixed order)
 // Unconditional, unrolled stream over the row's contiguous slots.  Multi-GPU:
@@ -1761,6 +1874,33 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym_near(
   near_row<double, NL, true>(e, threadIdx.x & 31, near_rs, near_b, blk, x, rows_out, l2g, sg);
 }
 
+// Leaf-level column-stream far field fused with the near rows (single GPU): as
+// k_far_sym_near, with far_col_body for the far part.
+template <int M, int NL, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_far_col_near(
+    int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
+    int leaf_off, const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+    const int* __restrict__ far_b, const int* __restrict__ trans, const double* __restrict__ img,
+    const double* __restrict__ up, double* __restrict__ down, double* __restrict__ slot,
+    const unsigned char* __restrict__ /*owned: single GPU*/, const int* __restrict__ near_rs,
+    const int* __restrict__ near_b, const double* __restrict__ blk, const double* __restrict__ x,
+    double* __restrict__ rows_out, const int* __restrict__ l2g, const double* __restrict__ sg) {
+  __shared__ __align__(16) double sh[8][(5 * M * M + 1) / 2 * 2];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  int e;
+  if (warp < n_fine) {
+    const int t = fine[warp];
+    far_col_body<M>(t, lane, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img, up, down, slot);
+    e = (t / npp) * epp + (t % npp - leaf_off);
+  } else if (warp < n_fine + n_rest) {
+    e = rest[warp - n_fine];
+  } else {
+    return;
+  }
+  near_row<double, NL, true>(e, lane, near_rs, near_b, blk, x, rows_out, l2g, sg);
+}
+
 // leaf backward transform moments^T down + near rows (h2.cpp:359-371); one
 // thread per (owned element, local function)
 template <class S, int NL>
@@ -1891,10 +2031,20 @@ static cudaMemPool_t device_pool(int device) {
   props.location.id = device;
   cudaMemPool_t pool;
   IGB_CUDA(cudaMemPoolCreate(&pool, &props));
+  // IGB_POOL_KEEP_MB bounds what stays reserved between operators (default:
+  // everything); igb_release_device_memory() trims it on demand
   uint64_t keep = UINT64_MAX;
+  if (const char* e = std::getenv("IGB_POOL_KEEP_MB")) keep = std::strtoull(e, nullptr, 10) << 20;
   IGB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   pools[device] = pool;
   return pool;
+}
+
+void release_device_memory(int device) {
+  cudaMemPool_t pool = device_pool(device);
+  IGB_CUDA(cudaSetDevice(device));
+  IGB_CUDA(cudaDeviceSynchronize());
+  IGB_CUDA(cudaMemPoolTrimTo(pool, 0));
 }
 
 // Pinned host staging buffers of the host-vector apply, recycled across
@@ -2011,6 +2161,7 @@ H2Device::~H2Device() {
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (ev_fork2_) cudaEventDestroy(ev_fork2_);
   if (ev_join2_) cudaEventDestroy(ev_join2_);
+  if (ev_apply_done_) cudaEventDestroy(ev_apply_done_);
   if (side_) cudaStreamDestroy(side_);
   if (side2_) cudaStreamDestroy(side2_);
   if (aux_) cudaStreamDestroy(aux_);
@@ -2102,6 +2253,8 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   IGB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   IGB_CUDA(cudaEventCreateWithFlags(&ev_fork2_, cudaEventDisableTiming));
   IGB_CUDA(cudaEventCreateWithFlags(&ev_join2_, cudaEventDisableTiming));
+  IGB_CUDA(cudaEventCreateWithFlags(&ev_apply_done_, cudaEventDisableTiming));
+  IGB_CUDA(cudaEventRecord(ev_apply_done_, stream_));
   IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -2235,6 +2388,12 @@ void H2Device::stage_plan() {
     d_far_targets_ = upload(targets);
     // symmetric fused far field (Laplace, m <= 6): upper pairs + transposes
     sym_far_ = !stored_couplings() && d.kind() == kLaplace && m >= 2 && m <= 6;
+    {
+      const char* fk = std::getenv("IGB_FAR_KERNEL");
+      far_col_ = sym_far_ && m <= 5 && Lp.world == 1 && !(fk && std::strcmp(fk, "tile") == 0);
+      const char* fm = std::getenv("IGB_FAR_COL_MINB");
+      far_col_minb_ = fm ? std::atoi(fm) : 3;
+    }
     // other kinds / larger m, one GPU: the warp-row symmetric kernel
     sym_w_ = !stored_couplings() && !sym_far_ && Lp.world == 1 && mm >= 32 && mm <= 128;
     if (sym_far_ || sym_w_) {
@@ -2261,6 +2420,8 @@ void H2Device::stage_plan() {
       for (int t : sym_targets) (P.node_level[t] == P.depth ? fine : coarse).push_back(t);
       n_sym_fine_ = static_cast<int>(fine.size());
       n_sym_coarse_ = static_cast<int>(coarse.size());
+      for (int t : fine) sym_pairs_[0] += P.far_row_start[t + 1] - P.far_upper_start[t];
+      for (int t : coarse) sym_pairs_[1] += P.far_row_start[t + 1] - P.far_upper_start[t];
       d_sym_fine_ = upload(fine);
       d_sym_coarse_ = upload(coarse);
       // fused leaf far field + near rows (single GPU, m = 4): the elements whose
@@ -2455,6 +2616,9 @@ void H2Device::run_assembly() {
 
 double H2Device::reassemble() {
   IGB_CUDA(cudaSetDevice(device_));
+  // the assembly rewrites the operator arrays: matvecs queued on any stream
+  // (apply_device on a caller's stream, DistH2Matrix phases) must finish first
+  IGB_CUDA(cudaDeviceSynchronize());
   dispatch_kind([&](auto kt) { run_assembly<decltype(kt)>(); });
   return times_.total_device;
 }
@@ -2693,7 +2857,7 @@ void H2Device::enqueue_apply(const double* xin, double* yout, cudaStream_t s, cu
 // transform, gather.  Side stream 2, concurrently: upward pass, coarse-level
 // far field + slots, downward levels above the leaves.  Side stream 1: near rows.
 template <class KT>
-void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t s) {
+void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t s, KernelMarks* prof) {
   using S = typename KT::S;
   constexpr int NL = KT::NL;
   const Discretization& d = *disc_;
@@ -2715,23 +2879,55 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   (void)nloc;
   (void)coef;
   const bool fused = KT::KIND == 0 && NL <= 16 && n_near_rest_ >= 0;
-  IGB_CUDA(cudaEventRecord(ev_fork_, s));
-  IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+  // profiling (prof != nullptr): the same kernels serialised on s, an event
+  // after each one, so every graph kernel is timed on its own
+  cudaStream_t side1 = prof ? s : side_, side2 = prof ? s : side2_;
+  auto tick = [&](const char* name) {
+    if (!prof) return;
+    cudaEvent_t e;
+    IGB_CUDA(cudaEventCreate(&e));
+    IGB_CUDA(cudaEventRecord(e, s));
+    prof->emplace_back(name, e);
+  };
+  tick("start");
+  if (!prof) {
+    IGB_CUDA(cudaEventRecord(ev_fork_, s));
+    IGB_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+  }
   if (!fused) {
-    k_near_rows<S, NL, true><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
+    k_near_rows<S, NL, true><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side1>>>(
         nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), x, nrows, d_l2g_, d_lsign_);
     ++launches;
+    tick("near_rows");
   }
-  IGB_CUDA(cudaEventRecord(ev_join_, side_));
+  if (!prof) IGB_CUDA(cudaEventRecord(ev_join_, side_));
   const long long ndown = static_cast<long long>(P.n_nodes) * rows;
   pdl_launch(k_leaf_up_x<S, NL>, grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s, 
       nel, rows, epp, npp, P.level_offset[L], d_mom_, x, d_l2g_, d_lsign_, up, down, ndown);
   ++launches;
-  IGB_CUDA(cudaEventRecord(ev_fork2_, s));
-  IGB_CUDA(cudaStreamWaitEvent(side2_, ev_fork2_, 0));
+  tick("leaf_up");
+  if (!prof) {
+    IGB_CUDA(cudaEventRecord(ev_fork2_, s));
+    IGB_CUDA(cudaStreamWaitEvent(side2_, ev_fork2_, 0));
+  }
   auto far_sym = [&](cudaStream_t st, int n, const int* targets) {
     if (n == 0) return;
     const unsigned g = grid_for(static_cast<long long>(n) * 32, 256);
+    if (far_col_ && m <= 5) {
+      switch (m) {
+        case 2: k_far_col<2, 4><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        case 3: k_far_col<3, 4><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        case 4: k_far_col<4, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        default:
+          if (far_col_minb_ == 2)
+            k_far_col<5, 2><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
+          else
+            k_far_col<5, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
+          break;
+      }
+      ++launches;
+      return;
+    }
     switch (m) {
       case 2: k_far_sym<2, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
       case 3: k_far_sym<3, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
@@ -2749,19 +2945,23 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   // side stream 2: upward pass, coarse far field, downward levels 0 .. L-2
   for (int l = L - 1; l >= 0; --l) {
     const long long tot = (l == 0 ? static_cast<long long>(np) : static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * (l - 1)))) * rows;
-    launch_up_level<S>(grid_for(tot, 256), side2_, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+    launch_up_level<S>(grid_for(tot, 256), side2, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
                        d_tl_, d_tr_, up, l == 0 ? 0 : Lp.c0, l == 0 ? 0 : Lp.c1);
     ++launches;
   }
-  far_sym(side2_, n_sym_coarse_, d_sym_coarse_);
-  far_lower(side2_, 2);
+  tick("upward");
+  far_sym(side2, n_sym_coarse_, d_sym_coarse_);
+  tick("far_coarse");
+  far_lower(side2, 2);
+  tick("far_lower_coarse");
   for (int l = 0; l + 1 < L; ++l) {
     const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
-    launch_down_level<S>(grid_for(tot, 256), side2_, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+    launch_down_level<S>(grid_for(tot, 256), side2, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
                          d_tl_, d_tr_, down, Lp.c0, Lp.c1);
     ++launches;
   }
-  IGB_CUDA(cudaEventRecord(ev_join2_, side2_));
+  tick("downward_coarse");
+  if (!prof) IGB_CUDA(cudaEventRecord(ev_join2_, side2_));
   // main: leaf-level far field (fused with the near rows when enabled)
   if (fused) {
     if constexpr (KT::KIND == 0 && NL <= 16) {
@@ -2773,7 +2973,13 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
             reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
             reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
       };
-      if (m == 4)
+      if (far_col_ && m == 4)
+        fused_launch(k_far_col_near<4, NL, 3>);
+      else if (far_col_ && far_col_minb_ == 2)
+        fused_launch(k_far_col_near<5, NL, 2>);
+      else if (far_col_)
+        fused_launch(k_far_col_near<5, NL, 3>);
+      else if (m == 4)
         fused_launch(k_far_sym_near<4, NL, IGB_M4_MINB>);
       else
         fused_launch(k_far_sym_near<5, NL, IGB_M5_MINB>);
@@ -2782,8 +2988,10 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   } else {
     far_sym(s, n_sym_fine_, d_sym_fine_);
   }
+  tick(fused ? "far_leaf_near" : "far_leaf");
   far_lower(s, 1);
-  IGB_CUDA(cudaStreamWaitEvent(s, ev_join2_, 0));
+  tick("far_lower_leaf");
+  if (!prof) IGB_CUDA(cudaStreamWaitEvent(s, ev_join2_, 0));
   {
     const int l = L - 1;
     const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
@@ -2791,11 +2999,14 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
                          d_tl_, d_tr_, down, Lp.c0, Lp.c1);
     ++launches;
   }
-  IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+  tick("downward_leaf");
+  if (!prof) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
   pdl_launch(k_leaf_down<S, NL>, grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s, 
       nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
+  tick("leaf_down");
   pdl_launch(k_scatter<S>, grid_for(d.dof_count(), 256), 256, 0, s, d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
   launches += 2;
+  tick("scatter");
   IGB_CUDA(cudaGetLastError());
   apply_launches_ = launches;
 }
@@ -2939,6 +3150,28 @@ void H2Device::profile_apply(int iters, double* phase_ms) {
   for (auto& e : ev) cudaEventDestroy(e);
 }
 
+std::vector<std::pair<std::string, double>> H2Device::profile_kernels(int iters) {
+  IGB_CUDA(cudaSetDevice(device_));
+  if (!split_graph()) throw std::logic_error("profile_kernels: only the single-GPU level-split graph");
+  std::vector<std::pair<std::string, double>> out;
+  for (int it = 0; it < iters; ++it) {
+    KernelMarks marks;
+    dispatch_kind([&](auto kt) {
+      if constexpr (decltype(kt)::KIND == 0) enqueue_apply_split<decltype(kt)>(dx_, dy_, stream_, &marks);
+    });
+    IGB_CUDA(cudaStreamSynchronize(stream_));
+    if (out.empty())
+      for (size_t k = 1; k < marks.size(); ++k) out.emplace_back(marks[k].first, 0.0);
+    for (size_t k = 1; k < marks.size(); ++k) {
+      float ms = 0;
+      IGB_CUDA(cudaEventElapsedTime(&ms, marks[k - 1].second, marks[k].second));
+      out[k - 1].second += ms;
+    }
+    for (auto& mk : marks) cudaEventDestroy(mk.second);
+  }
+  return out;
+}
+
 double H2Device::bench_steps(int steps, int matvecs, double* assembly_ms) {
   IGB_CUDA(cudaSetDevice(device_));
   launch_apply_graph(stream_);  // instantiate outside the timed region
@@ -2966,9 +3199,13 @@ void H2Device::apply_device(const double* x, double* y, cudaStream_t s) {
   const size_t bytes = static_cast<size_t>(dim()) * (is_complex() ? 16 : 8);
   IGB_CUDA(cudaSetDevice(device_));
   if (s == nullptr) s = stream_;
+  // dx_ / dy_ are shared by every apply on this handle: order this call after
+  // the previous one, whichever stream that ran on
+  IGB_CUDA(cudaStreamWaitEvent(s, ev_apply_done_, 0));
   IGB_CUDA(cudaMemcpyAsync(dx_, x, bytes, cudaMemcpyDeviceToDevice, s));
   launch_apply_graph(s);
   IGB_CUDA(cudaMemcpyAsync(y, dy_, bytes, cudaMemcpyDeviceToDevice, s));
+  IGB_CUDA(cudaEventRecord(ev_apply_done_, s));
 }
 
 void H2Device::apply_host(const double* x, double* y) {
@@ -2979,14 +3216,18 @@ void H2Device::apply_host(const double* x, double* y) {
     h_y_pinned_ = static_cast<double*>(pinned_get(bytes));
   }
   std::memcpy(h_x_pinned_, x, bytes);
+  IGB_CUDA(cudaStreamWaitEvent(stream_, ev_apply_done_, 0));  // a device apply on another stream
   IGB_CUDA(cudaMemcpyAsync(dx_, h_x_pinned_, bytes, cudaMemcpyHostToDevice, stream_));
   launch_apply_graph(stream_);
   IGB_CUDA(cudaMemcpyAsync(h_y_pinned_, dy_, bytes, cudaMemcpyDeviceToHost, stream_));
+  IGB_CUDA(cudaEventRecord(ev_apply_done_, stream_));
   IGB_CUDA(cudaStreamSynchronize(stream_));
   std::memcpy(y, h_y_pinned_, bytes);
 }
 
 void H2Device::near_blocks(long long first, long long count, double* out) const {
+  if (lp_.world > 1)  // a rank holds only its own block rows, in a rank-local layout
+    throw std::logic_error("near_blocks: not available on a rank of a distributed operator");
   const int nl = disc_->local_count(), sw = is_complex() ? 2 : 1;
   if (first < 0 || first + count > static_cast<long long>(plan_.near_a.size()))
     throw std::invalid_argument("near_blocks: range out of bounds");
@@ -3009,6 +3250,8 @@ void H2Device::near_blocks(long long first, long long count, double* out) const 
   }
 }
 void H2Device::couplings(long long first, long long count, double* out) const {
+  if (lp_.world > 1)
+    throw std::logic_error("couplings: not available on a rank of a distributed operator");
   const size_t per = static_cast<size_t>(plan_.m) * plan_.m * plan_.m * plan_.m * (is_complex() ? 2 : 1);
   if (first < 0 || first + count > static_cast<long long>(plan_.far_a.size()))
     throw std::invalid_argument("couplings: range out of bounds");

@@ -5,6 +5,8 @@
 
 #include <chrono>
 #include <memory>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "igb_host.hpp"
@@ -65,6 +67,11 @@ class H2Device {
   // per-phase matvec time (ms summed over iters): coef, leaf_up, upward,
   // zero, far, downward, near_leaf, scatter
   void profile_apply(int iters, double* phase_ms);
+  // the level-split matvec graph's kernels launched one after another on the
+  // handle's stream, each timed with CUDA events: (name, ms summed over iters)
+  std::vector<std::pair<std::string, double>> profile_kernels(int iters);
+  // unordered far pairs the symmetric far kernels evaluate: [leaf level, above]
+  long long sym_pairs(int which) const { return sym_pairs_[which]; }
   // `steps` x (device assembly + `matvecs` matvecs), CUDA events; returns ms
   double bench_steps(int steps, int matvecs, double* assembly_ms);
   int assembly_kernel_launches() const { return assembly_kernels_; }
@@ -89,7 +96,8 @@ class H2Device {
   enum { kEvStart, kEvElements, kEvCoincident, kEvEdge, kEvVertex, kEvUploaded, kEvPlanPhase, kEvImages,
          kEvCouplings, kEvRegular, kEvScatter, kAsmEvents };
   template <class KT> void enqueue_apply(const double* x, double* y, cudaStream_t s, cudaEvent_t* pev);
-  template <class KT> void enqueue_apply_split(const double* x, double* y, cudaStream_t s);
+  using KernelMarks = std::vector<std::pair<const char*, cudaEvent_t>>;
+  template <class KT> void enqueue_apply_split(const double* x, double* y, cudaStream_t s, KernelMarks* prof = nullptr);
   // the single-GPU symmetric far field is captured as the level-split graph
   bool split_graph() const { return sym_far_ && lp_.world == 1 && plan_.depth >= 1; }
   template <class KT> void enqueue_phase1(const double* x, double* send, cudaStream_t s, cudaEvent_t* pev, int& n);
@@ -136,9 +144,12 @@ class H2Device {
   int n_far_targets_ = 0;
   bool sym_far_ = false;  // Laplace m <= 6: lane-tile symmetric far kernel
   bool sym_w_ = false;    // other kinds / m, one GPU: warp-row symmetric far kernel
+  bool far_col_ = false;  // Laplace m <= 5, one GPU: column-stream far kernel (k_far_col)
+  int far_col_minb_ = 3;
   int n_sym_targets_ = 0;
   int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;
   int n_sym_fine_ = 0, n_sym_coarse_ = 0;  // leaf-level / coarser symmetric targets
+  long long sym_pairs_[2] = {0, 0};        // unordered far pairs evaluated by them
   int *d_sym_fine_ = nullptr, *d_sym_coarse_ = nullptr;
   int n_near_rest_ = -1;  // fused leaf far field + near rows: elements without leaf targets (-1: off)
   int* d_near_rest_ = nullptr;
@@ -163,6 +174,7 @@ class H2Device {
   double* d_nrows_ = nullptr;
   cudaStream_t side_ = nullptr, side2_ = nullptr;
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_fork2_ = nullptr, ev_join2_ = nullptr;
+  cudaEvent_t ev_apply_done_ = nullptr;  // last apply's final copy (dx_/dy_ hand-off between streams)
   cudaGraphExec_t graph_exec_ = nullptr;
   cudaGraphExec_t graph1_ = nullptr, graph2_ = nullptr;  // multi-GPU phases
   bool near_in_phase2_ = false;  // set while capturing the phase graphs
@@ -178,6 +190,9 @@ class H2Device {
     double kp[4] = {0, 0, 0, 0};
   } as_;
 };
+
+// return the memory of destroyed operators (kept reserved for re-use) to the driver
+void release_device_memory(int device);
 
 // Dense Galerkin matrix (assembly.cpp:16-53) on one device; `out`: host,
 // column-major dof_count^2 Scalar (interleaved complex for Helmholtz/Maxwell)

@@ -91,6 +91,7 @@ SYMBOLS = (
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_create_ex", "igb_plan_counts", "igb_plan_near_pairs",
     "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
     "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
+    "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work",
 )
 
 
@@ -169,6 +170,9 @@ def lib():
     L.igb_dense_assemble.argtypes = [vp, i32, i32, i32, P(f64)]
     L.igb_admissible.argtypes = [P(f64), P(f64), f64]
     L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
+    L.igb_release_device_memory.argtypes = [i32]
+    L.igb_h2_far_work.argtypes = [vp, P(i64)]
+    L.igb_h2_profile_kernels.argtypes = [vp, i32, i32, ctypes.c_char_p, P(f64), P(i32)]
     _LIB = L
     return L
 
@@ -571,6 +575,26 @@ class H2Matrix:
         out = np.zeros(8)
         _check(lib().igb_h2_profile_apply(self._h, int(iters), _p(out)))
         return dict(zip(self.PHASES, out.tolist()))
+
+    def profile_kernels(self, iters=10):
+        """The matvec graph's own kernels, serialised, each timed with CUDA
+        events: {role: ms summed over iters} (single-GPU level-split graph)."""
+        names = ctypes.create_string_buffer(64 * 32)
+        ms = np.zeros(64)
+        n = ctypes.c_int()
+        _check(lib().igb_h2_profile_kernels(self._h, int(iters), 64, names, _p(ms), ctypes.byref(n)))
+        out = {}
+        for k in range(n.value):
+            key = names.raw[32 * k:32 * (k + 1)].split(b"\0")[0].decode()
+            out[key] = out.get(key, 0.0) + float(ms[k])
+        return out
+
+    def far_sym_counts(self):
+        """unordered far pairs evaluated per matvec by the symmetric far kernels:
+        {'leaf': leaf level, 'coarse': above it}"""
+        out = np.zeros(2, dtype=np.int64)
+        _check(lib().igb_h2_far_work(self._h, _p(out, ctypes.c_longlong)))
+        return dict(leaf=int(out[0]), coarse=int(out[1]))
 
     def bench_steps(self, steps, matvecs):
         """steps x (device assembly + matvecs matvecs): (total ms, assembly ms) from CUDA events."""
