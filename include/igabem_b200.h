@@ -172,6 +172,12 @@ int igb_h2_profile_kernels(igb_h2* h, int iters, int max_n, char* names, double*
 /* unordered far pairs the symmetric far-field kernels evaluate per matvec:
  * pairs[0] on the leaf level, pairs[1] above it (0, 0 for other far kernels) */
 int igb_h2_far_work(const igb_h2* h, long long pairs[2]);
+/* introspection of the far field (phase 4 of H2Matrix::apply, h2.cpp:312-326):
+ * runs the matvec on host x through the upward pass and the far field (with
+ * the kernel the matvec uses), then copies up and down, each
+ * [node][c*m^2 + nu] Scalar (node_count * nch * m^2 scalars); either may be
+ * NULL.  Single-GPU handles only. */
+int igb_h2_far_field(igb_h2* h, const double* x, double* up, double* down);
 /* `steps` x (device assembly + `matvecs` matvecs) on the handle stream,
  * CUDA-event timed; *total_ms, *assembly_ms (sum of assembly device time) */
 int igb_h2_bench_steps(igb_h2* h, int steps, int matvecs, double* total_ms, double* assembly_ms);

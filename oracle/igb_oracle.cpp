@@ -1495,7 +1495,10 @@ struct H2 : H2Base {
   std::vector<int> near_row_start, far_row_start;
   std::vector<std::vector<V3>> images;
 
-  // h2.cpp:99-129; flags bit0: skip near quadrature (zero blocks), bit1: skip couplings
+  // h2.cpp:99-129; flags bit0: skip near quadrature (zero blocks), bit1: skip couplings,
+  // bit2: couplings evaluated where used (never stored; same formula, bitwise
+  // equal), bit3: near blocks integrated where used (never stored) -- bits 2/3
+  // let probe() check full-size configurations whose operator does not fit
   H2(const Disc& d, int m_, double eta_, int fo, int so, int flags)
       : disc(&d), m(m_), eta(eta_), far_order(fo), sing_order(so), tree(d), dim(d.n_dofs) {
     if (m < 2) throw std::invalid_argument("H2Matrix: interpolation degree m < 2");
@@ -1599,17 +1602,22 @@ struct H2 : H2Base {
     std::sort(near_pairs.begin(), near_pairs.end());
     std::sort(far_pairs.begin(), far_pairs.end());
 
-    coupling.resize(far_pairs.size());
+    lazy_far = (flags & 4) != 0;
+    lazy_near = (flags & 8) != 0;
+    near_row_start.assign(disc->ne() + 1, 0);
+    for (const auto& pr : near_pairs) ++near_row_start[pr.first + 1];
+    for (int e = 0; e < disc->ne(); ++e) near_row_start[e + 1] += near_row_start[e];
+    far_row_start.assign(nn + 1, 0);
+    for (const auto& pr : far_pairs) ++far_row_start[pr.first + 1];
+    for (int t = 0; t < nn; ++t) far_row_start[t + 1] += far_row_start[t];
+    if (!lazy_far) coupling.resize(far_pairs.size());
 #pragma omp parallel for schedule(dynamic, 64)
-    for (size_t q = 0; q < far_pairs.size(); ++q) {
-      const auto [ta, tb] = far_pairs[q];
+    for (size_t q = 0; q < coupling.size(); ++q) {
       Mat<S> k(mm, mm);
-      if (!(flags & 2))
-        for (int mu = 0; mu < mm; ++mu)
-          for (int nu = 0; nu < mm; ++nu)
-            k(nu, mu) = kernel_g<S>(*disc, norm(images[ta][nu] - images[tb][mu]));
+      if (!(flags & 2)) k = make_coupling(q);
       coupling[q] = std::move(k);
     }
+    if (lazy_near) return;
     const int nfar = disc->resolved_far(far_order);
     const int nsing = disc->resolved_sing(sing_order);
     const int ne = disc->ne();
@@ -1627,16 +1635,41 @@ struct H2 : H2Base {
       else
         near_blk[q] = pair_block<S>(*disc, caches, ea, eb, nsing);
     }
-    near_row_start.assign(ne + 1, 0);
-    for (const auto& pr : near_pairs) ++near_row_start[pr.first + 1];
-    for (int e = 0; e < ne; ++e) near_row_start[e + 1] += near_row_start[e];
-    far_row_start.assign(nn + 1, 0);
-    for (const auto& pr : far_pairs) ++far_row_start[pr.first + 1];
-    for (int t = 0; t < nn; ++t) far_row_start[t + 1] += far_row_start[t];
   }
 
-  // h2.cpp:254-378
-  void apply(const S* x, S* y) const {
+  bool lazy_far = false, lazy_near = false;
+  // K[nu, mu] = G(|img_ta[nu] - img_tb[mu]|) (h2.cpp:218-229)
+  Mat<S> make_coupling(size_t q) const {
+    const int mm = m * m;
+    const auto [ta, tb] = far_pairs[q];
+    Mat<S> k(mm, mm);
+    for (int mu = 0; mu < mm; ++mu)
+      for (int nu = 0; nu < mm; ++nu) k(nu, mu) = kernel_g<S>(*disc, norm(images[ta][nu] - images[tb][mu]));
+    return k;
+  }
+  const Mat<S>& coupling_at(size_t q, Mat<S>& tmp) const {
+    if (!lazy_far) return coupling[q];
+    tmp = make_coupling(q);
+    return tmp;
+  }
+  // near block of pair q (stored, or integrated now: h2.cpp:236-243)
+  Mat<S> near_block_at(size_t q) const {
+    if (!lazy_near) return near_blk[q];
+    const auto [ea, eb] = near_pairs[q];
+    thread_local std::vector<FarCache<S>> caches;  // per thread, only the pair's two entries filled
+    if (caches.size() != static_cast<size_t>(disc->ne())) caches.assign(disc->ne(), FarCache<S>{});
+    const int nfar = disc->resolved_far(far_order);
+    caches[ea] = make_far_cache<S>(*disc, ea, nfar);
+    if (eb != ea) caches[eb] = make_far_cache<S>(*disc, eb, nfar);
+    Mat<S> b = pair_block<S>(*disc, caches, ea, eb, disc->resolved_sing(sing_order));
+    caches[ea] = FarCache<S>{};
+    caches[eb] = FarCache<S>{};
+    return b;
+  }
+
+  // h2.cpp:254-378; optional outputs: up (phase 3), down after the far field
+  // (phase 4) and after the downward pass (phase 5), each [node][c*m^2 + nu]
+  void apply(const S* x, S* y, S* up_out = nullptr, S* down4_out = nullptr, S* down5_out = nullptr) const {
     const int mm = m * m;
     const int ne = disc->ne(), nl = disc->n_local;
     const int nn = static_cast<int>(tree.nodes.size());
@@ -1704,8 +1737,9 @@ struct H2 : H2Base {
       if (far_row_start[t] == far_row_start[t + 1]) continue;
       has_down[t] = 1;
       S* acc = &down[static_cast<size_t>(t) * ncol];
+      Mat<S> ktmp;
       for (int q = far_row_start[t]; q < far_row_start[t + 1]; ++q) {
-        const Mat<S>& K = coupling[q];
+        const Mat<S>& K = coupling_at(q, ktmp);
         const S* src = &up[static_cast<size_t>(far_pairs[q].second) * ncol];
         for (int c = 0; c < nch; ++c) {
           const S w = (vec && c == 3) ? divw : S(1);
@@ -1718,6 +1752,8 @@ struct H2 : H2Base {
         }
       }
     }
+    if (up_out) std::copy(up.begin(), up.end(), up_out);
+    if (down4_out) std::copy(down.begin(), down.end(), down4_out);
     for (int l = 0; l < depth; ++l) {
       const int n = 2 << l;
 #pragma omp parallel for schedule(static) collapse(2)
@@ -1735,12 +1771,13 @@ struct H2 : H2Base {
                    &down[static_cast<size_t>(id) * ncol + c * mm], true);
         }
     }
+    if (down5_out) std::copy(down.begin(), down.end(), down5_out);
     std::vector<S> near_rows(static_cast<size_t>(ne) * nl, S(0));
 #pragma omp parallel for schedule(dynamic)
     for (int e = 0; e < ne; ++e) {
       S* acc = &near_rows[static_cast<size_t>(e) * nl];
       for (int q = near_row_start[e]; q < near_row_start[e + 1]; ++q) {
-        const Mat<S>& B = near_blk[q];
+        const Mat<S> B = near_block_at(q);
         const S* c = &coef[static_cast<size_t>(near_pairs[q].second) * nl];
         for (int lb = 0; lb < nl; ++lb)
           for (int la = 0; la < nl; ++la) acc[la] += B(la, lb) * c[lb];
@@ -1770,6 +1807,152 @@ struct H2 : H2Base {
           }
         }
     }
+  }
+
+  // Selected outputs of apply() without the full operator: up (all nodes), the
+  // phase-4 down of `nodes`, and y at `dofs`.  Only what they depend on is
+  // evaluated -- the full upward pass, the far rows of the selected nodes and of
+  // the ancestors of the selected DOFs' leaves, the near rows of their elements
+  // -- with apply()'s arithmetic in apply()'s order, so every value equals
+  // apply()'s bitwise.  With lazy couplings / near blocks (flags bits 2, 3) this
+  // checks full-size configurations whose operator does not fit host memory.
+  void probe(const S* x, S* up_out, int n_nodes, const int* nodes, S* down4_out, int n_dofs, const int* dofs,
+             S* y_out) const {
+    const int mm = m * m, ncol = mm * nch;
+    const int ne = disc->ne(), nl = disc->n_local, nn = static_cast<int>(tree.nodes.size());
+    const int depth = tree.depth, np = disc->geom->patch_count();
+    const bool vec = disc->is_vector();
+    S divw(0);
+    if constexpr (std::is_same_v<S, cplx>) {
+      if (vec) divw = -1.0 / (disc->kappa * disc->kappa);
+    }
+    std::vector<S> coef(static_cast<size_t>(ne) * nl);
+#pragma omp parallel for schedule(static)
+    for (int e = 0; e < ne; ++e)
+      for (int l = 0; l < nl; ++l) {
+        const size_t i = static_cast<size_t>(e) * nl + l;
+        coef[i] = S(disc->lsign[i]) * x[disc->l2g[i]];
+      }
+    std::vector<S> up(static_cast<size_t>(nn) * ncol, S(0));
+#pragma omp parallel for schedule(static)
+    for (int id = 0; id < nn; ++id) {
+      if (!tree.is_leaf(id)) continue;
+      const int e = tree.leaf_element(id);
+      const Mat<S>& mo = moments[e];
+      for (int r = 0; r < mo.r; ++r) {
+        S acc(0);
+        for (int l = 0; l < nl; ++l) acc += mo(r, l) * coef[static_cast<size_t>(e) * nl + l];
+        up[static_cast<size_t>(id) * ncol + r] = acc;
+      }
+    }
+    auto add_tx = [&](const Mat<S>& tu, const Mat<S>& tv, const S* X, S* Y, bool transpose) {
+      std::vector<S> tmp(mm, S(0));
+      for (int j = 0; j < m; ++j)
+        for (int k = 0; k < m; ++k) {
+          const S xk = X[k + m * j];
+          for (int i = 0; i < m; ++i) tmp[i + m * j] += (transpose ? tu(k, i) : tu(i, k)) * xk;
+        }
+      for (int j = 0; j < m; ++j)
+        for (int k = 0; k < m; ++k) {
+          const S t = transpose ? tv(k, j) : tv(j, k);
+          for (int i = 0; i < m; ++i) Y[i + m * j] += tmp[i + m * k] * t;
+        }
+    };
+    for (int l = depth - 1; l >= 0; --l) {
+      const int n = 1 << l;
+#pragma omp parallel for schedule(static) collapse(2)
+      for (int p = 0; p < np; ++p)
+        for (int sq = 0; sq < n * n; ++sq) {
+          const int id = tree.node_id(p, l, sq % n, sq / n);
+          S* Y = &up[static_cast<size_t>(id) * ncol];
+          for (int k = 0; k < 4; ++k) {
+            const S* X = &up[static_cast<size_t>(tree.child(id, k)) * ncol];
+            const Mat<S>& tu = (k & 1) ? tr : tl;
+            const Mat<S>& tv = (k >> 1) ? tr : tl;
+            for (int c = 0; c < nch; ++c) add_tx(tu, tv, X + c * mm, Y + c * mm, false);
+          }
+        }
+    }
+    if (up_out) std::copy(up.begin(), up.end(), up_out);
+    // phase-4 row of node t (the far loop of apply())
+    auto down4 = [&](int t, S* acc) {
+      for (int i = 0; i < ncol; ++i) acc[i] = S(0);
+      Mat<S> ktmp;
+      for (int q = far_row_start[t]; q < far_row_start[t + 1]; ++q) {
+        const Mat<S>& K = coupling_at(q, ktmp);
+        const S* src = &up[static_cast<size_t>(far_pairs[q].second) * ncol];
+        for (int c = 0; c < nch; ++c) {
+          const S w = (vec && c == 3) ? divw : S(1);
+          std::vector<S> kx(mm, S(0));
+          for (int mu = 0; mu < mm; ++mu) {
+            const S xm = src[c * mm + mu];
+            for (int nu = 0; nu < mm; ++nu) kx[nu] += K(nu, mu) * xm;
+          }
+          for (int nu = 0; nu < mm; ++nu) acc[c * mm + nu] += w * kx[nu];
+        }
+      }
+    };
+#pragma omp parallel for schedule(dynamic)
+    for (int k = 0; k < n_nodes; ++k) down4(nodes[k], down4_out + static_cast<size_t>(k) * ncol);
+    if (n_dofs == 0) return;
+    // elements touching the selected DOFs, ascending (apply()'s gather order)
+    std::vector<int> pos(disc->n_dofs, -1);
+    for (int k = 0; k < n_dofs; ++k) pos[dofs[k]] = k;
+    std::vector<int> els;
+    for (int e = 0; e < ne; ++e)
+      for (int l = 0; l < nl; ++l)
+        if (pos[disc->l2g[static_cast<size_t>(e) * nl + l]] >= 0) {
+          els.push_back(e);
+          break;
+        }
+    const int side = 1 << depth;
+    std::vector<std::vector<S>> loc(els.size());
+#pragma omp parallel for schedule(dynamic)
+    for (size_t i = 0; i < els.size(); ++i) {
+      const int e = els[i];
+      const int p = e / (side * side), sxe = e % side, sye = (e / side) % side;
+      // down along the root -> leaf path (apply()'s phase 5 restricted to it)
+      std::vector<S> dpar(ncol), dch(ncol);
+      int parent = tree.node_id(p, 0, 0, 0);
+      down4(parent, dpar.data());
+      bool has = far_row_start[parent] < far_row_start[parent + 1];
+      for (int l = 0; l < depth; ++l) {
+        const int sh = depth - l - 1, sx = sxe >> sh, sy = sye >> sh;
+        const int id = tree.node_id(p, l + 1, sx, sy);
+        down4(id, dch.data());
+        const bool own = far_row_start[id] < far_row_start[id + 1];
+        if (has) {
+          const Mat<S>& tu = (sx & 1) ? tr : tl;
+          const Mat<S>& tv = (sy & 1) ? tr : tl;
+          for (int c = 0; c < nch; ++c) add_tx(tu, tv, &dpar[c * mm], &dch[c * mm], true);
+        }
+        has = has || own;
+        std::swap(dpar, dch);
+      }
+      std::vector<S> lc(nl, S(0));
+      for (int q = near_row_start[e]; q < near_row_start[e + 1]; ++q) {
+        const Mat<S> B = near_block_at(q);
+        const S* c = &coef[static_cast<size_t>(near_pairs[q].second) * nl];
+        for (int lb = 0; lb < nl; ++lb)
+          for (int la = 0; la < nl; ++la) lc[la] += B(la, lb) * c[lb];
+      }
+      if (has) {
+        const Mat<S>& mo = moments[e];
+        for (int l = 0; l < nl; ++l) {
+          S acc(0);
+          for (int r = 0; r < mo.r; ++r) acc += mo(r, l) * dpar[r];
+          lc[l] += acc;
+        }
+      }
+      loc[i] = std::move(lc);
+    }
+    for (int k = 0; k < n_dofs; ++k) y_out[k] = S(0);
+    for (size_t i = 0; i < els.size(); ++i)
+      for (int l = 0; l < nl; ++l) {
+        const size_t g = static_cast<size_t>(els[i]) * nl + l;
+        const int k = pos[disc->l2g[g]];
+        if (k >= 0) y_out[k] += S(disc->lsign[g]) * loc[i][l];
+      }
   }
 
   void storage(long long* out) const {  // h2.cpp:380-390
@@ -2093,6 +2276,31 @@ int orc_h2_apply(void* hp, const double* x, double* y) {
       h->real->apply(x, y);
     else
       h->cx->apply(reinterpret_cast<const cplx*>(x), reinterpret_cast<cplx*>(y));
+  });
+}
+// apply with internals: up, down after phase 4, down after phase 5 (any may be null)
+int orc_h2_apply_ex(void* hp, const double* x, double* y, double* up, double* down4, double* down5) {
+  return guard([&] {
+    OH2* h = static_cast<OH2*>(hp);
+    if (h->real) {
+      h->real->apply(x, y, up, down4, down5);
+    } else {
+      auto c = [](double* p) { return reinterpret_cast<cplx*>(p); };
+      h->cx->apply(reinterpret_cast<const cplx*>(x), c(y), c(up), c(down4), c(down5));
+    }
+  });
+}
+// probe: up (all nodes), phase-4 down of `nodes`, y at `dofs` (see H2::probe)
+int orc_h2_probe(void* hp, const double* x, double* up, int n_nodes, const int* nodes, double* down4, int n_dofs,
+                 const int* dofs, double* y) {
+  return guard([&] {
+    OH2* h = static_cast<OH2*>(hp);
+    if (h->real) {
+      h->real->probe(x, up, n_nodes, nodes, down4, n_dofs, dofs, y);
+    } else {
+      auto c = [](double* p) { return reinterpret_cast<cplx*>(p); };
+      h->cx->probe(reinterpret_cast<const cplx*>(x), c(up), n_nodes, nodes, c(down4), n_dofs, dofs, c(y));
+    }
   });
 }
 int orc_admissible(const double* boxa, const double* boxb, double eta) {

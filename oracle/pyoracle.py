@@ -79,6 +79,8 @@ def lib():
         _sig(L, "orc_pair_rule", [i32, i32, P(f64), P(i64)])
         _sig(L, "orc_admissible", [P(f64), P(f64), f64])
         # 8(f) pipeline: exported by the reference harness (oracle/_ref) only
+        _sig(L, "orc_h2_apply_ex", [vp, P(f64), P(f64), P(f64), P(f64), P(f64)], optional=True)
+        _sig(L, "orc_h2_probe", [vp, P(f64), P(f64), i32, P(i32), P(f64), i32, P(i32), P(f64)], optional=True)
         _sig(L, "orc_rhs", [vp, i32, P(f64), i32, P(f64)], optional=True)
         _sig(L, "orc_solve", [vp, i32, P(f64), f64, i32, i32, P(f64), P(f64)], optional=True)
         _sig(L, "orc_potential", [vp, P(f64), i32, P(f64), i32, P(f64)], optional=True)
@@ -258,6 +260,33 @@ class H2Matrix:
         return y
 
     __matmul__ = apply
+
+    def apply_ex(self, x):
+        """(y, up, down after the far field (phase 4), down after the downward
+        pass (phase 5)); up / down: (node_count, nch * m^2) (oracle only)"""
+        x = np.ascontiguousarray(x, dtype=self.dtype)
+        y = np.zeros_like(x)
+        shp = (self.node_count, self.nch * self.m * self.m)
+        up, d4, d5 = (np.zeros(shp, dtype=self.dtype) for _ in range(3))
+        _check(lib().orc_h2_apply_ex(self._h, _p(x.view(np.float64)), _p(y.view(np.float64)),
+                                     _p(up.view(np.float64)), _p(d4.view(np.float64)), _p(d5.view(np.float64))))
+        return y, up, d4, d5
+
+    def probe(self, x, nodes=(), dofs=()):
+        """(up of all nodes, phase-4 down of `nodes`, y at `dofs`) with apply()'s
+        arithmetic, evaluating only what they depend on (oracle only; with
+        flags bits 2/3 couplings / near blocks are computed where used)"""
+        x = np.ascontiguousarray(x, dtype=self.dtype)
+        nodes = np.ascontiguousarray(nodes, dtype=np.int32)
+        dofs = np.ascontiguousarray(dofs, dtype=np.int32)
+        ncol = self.nch * self.m * self.m
+        up = np.zeros((self.node_count, ncol), dtype=self.dtype)
+        d4 = np.zeros((max(len(nodes), 1), ncol), dtype=self.dtype)
+        y = np.zeros(max(len(dofs), 1), dtype=self.dtype)
+        _check(lib().orc_h2_probe(self._h, _p(x.view(np.float64)), _p(up.view(np.float64)), len(nodes),
+                                  _p(nodes, ctypes.c_int), _p(d4.view(np.float64)), len(dofs), _p(dofs, ctypes.c_int),
+                                  _p(y.view(np.float64))))
+        return up, d4[:len(nodes)], y[:len(dofs)]
 
     def solve(self, b, method="gmres", tol=1e-8, max_iter=1000, restart=30):
         """reference gmres / cg (solver.hpp) on this H2Matrix"""

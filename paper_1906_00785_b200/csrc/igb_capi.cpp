@@ -419,6 +419,13 @@ int igb_h2_profile_kernels(igb_h2* h, int iters, int max_n, char* names, double*
     }
   });
 }
+int igb_h2_far_field(igb_h2* h, const double* x, double* up, double* down) {
+  return guard([&] {
+    need(h, "h2");
+    need(x, "x");
+    h->dev->far_field(x, up, down);
+  });
+}
 int igb_h2_far_work(const igb_h2* h, long long pairs[2]) {
   return guard([&] {
     need(h, "h2");

@@ -1641,7 +1641,7 @@ __device__ __forceinline__ void col_reduce_rows(double (&acc)[ColRows<MM>::R], i
   }
 }
 
-template <int M>
+template <int M, int C>
 __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict__ sh,
                                              const int* __restrict__ upper_start, const int* __restrict__ far_rs,
                                              const int* __restrict__ far_b, const int* __restrict__ trans,
@@ -1667,40 +1667,54 @@ __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict
   for (int i = 0; i < R; ++i) acc[i] = 0.0;
   const int q0 = upper_start[t];
   const int ncol = (far_rs[t + 1] - q0) * MM;
-  for (int c0 = 0; c0 < ncol; c0 += 32) {
-    const int c = c0 + lane;
-    const bool ok = c < ncol;
-    const int qi = ok ? c / MM : 0, mu = ok ? c - qi * MM : 0;
-    const int q = q0 + qi;
-    const int s = ok ? __ldg(far_b + q) : t;
-    const double* p = img + (static_cast<size_t>(s) * MM + mu) * 3;
-    double sx = __ldg(p) - cx, sy = __ldg(p + 1) - cy, sz = __ldg(p + 2) - cz;
-    double xs = __ldg(up + static_cast<size_t>(s) * MM + mu);
-    if (!ok) {  // padding column: far away (finite kernel), zero weight
-      sx = 1.0e8;
-      sy = sz = 0.0;
-      xs = 0.0;
+  // C columns per lane: each broadcast target row feeds C evaluations
+  for (int c0 = 0; c0 < ncol; c0 += 32 * C) {
+    double sx[C], sy[C], sz[C], xs[C], ns[C], ps[C];
+    int q[C], mu[C];
+    bool ok[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int c = c0 + 32 * k + lane;
+      ok[k] = c < ncol;
+      const int qi = ok[k] ? c / MM : 0;
+      mu[k] = ok[k] ? c - qi * MM : 0;
+      q[k] = q0 + qi;
+      const int s = ok[k] ? __ldg(far_b + q[k]) : t;
+      const double* p = img + (static_cast<size_t>(s) * MM + mu[k]) * 3;
+      sx[k] = __ldg(p) - cx;
+      sy[k] = __ldg(p + 1) - cy;
+      sz[k] = __ldg(p + 2) - cz;
+      xs[k] = __ldg(up + static_cast<size_t>(s) * MM + mu[k]);
+      if (!ok[k]) {  // padding column: far away (finite kernel), zero weight
+        sx[k] = 1.0e8;
+        sy[k] = sz[k] = 0.0;
+        xs[k] = 0.0;
+      }
+      ns[k] = sx[k] * sx[k] + sy[k] * sy[k] + sz[k] * sz[k];
+      ps[k] = 0.0;
     }
-    const double ns = sx * sx + sy * sy + sz * sz;
-    double ps0 = 0.0, ps1 = 0.0;
 #pragma unroll
     for (int nu = 0; nu < MM; ++nu) {
       const double2 a01 = *reinterpret_cast<const double2*>(sh + 4 * nu);
       const double2 a23 = *reinterpret_cast<const double2*>(sh + 4 * nu + 2);
       const double xt = sh[4 * MM + nu];
-      const double r2 = fma(a01.x, sx, fma(a01.y, sy, fma(a23.x, sz, a23.y + ns)));
-      const double gk = far_rsqrt(r2);  // kFarScale * 4 pi G
-      acc[nu] = fma(gk, xs, acc[nu]);
-      if (nu & 1) ps1 = fma(gk, xt, ps1);
-      else ps0 = fma(gk, xt, ps0);
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const double r2 = fma(a01.x, sx[k], fma(a01.y, sy[k], fma(a23.x, sz[k], a23.y + ns[k])));
+        const double gk = far_rsqrt(r2);  // kFarScale * 4 pi G
+        acc[nu] = fma(gk, xs[k], acc[nu]);
+        ps[k] = fma(gk, xt, ps[k]);
+      }
     }
-    if (ok) slot[static_cast<size_t>(__ldg(trans + q)) * MM + mu] = (ps0 + ps1) * kFarScale;
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+      if (ok[k]) slot[static_cast<size_t>(__ldg(trans + q[k])) * MM + mu[k]] = ps[k] * kFarScale;
   }
   col_reduce_rows<MM>(acc, lane);
   if (lane < MM) down[static_cast<size_t>(t) * MM + lane] = acc[0] * kFarScale;
 }
 
-template <int M, int MINB>
+template <int M, int MINB, int C>
 __global__ void __launch_bounds__(256, MINB) k_far_col(int n_targets, const int* __restrict__ targets,
                                                       const int* __restrict__ upper_start,
                                                       const int* __restrict__ far_rs, const int* __restrict__ far_b,
@@ -1710,8 +1724,8 @@ __global__ void __launch_bounds__(256, MINB) k_far_col(int n_targets, const int*
   __shared__ __align__(16) double sh[8][(5 * M * M + 1) / 2 * 2];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= n_targets) return;
-  far_col_body<M>(targets[warp], threadIdx.x & 31, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img,
-                  up, down, slot);
+  far_col_body<M, C>(targets[warp], threadIdx.x & 31, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img,
+                     up, down, slot);
 }
 
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
@@ -1876,7 +1890,7 @@ __global__ void __launch_bounds__(256, MINB) k_far_sym_near(
 
 // Leaf-level column-stream far field fused with the near rows (single GPU): as
 // k_far_sym_near, with far_col_body for the far part.
-template <int M, int NL, int MINB>
+template <int M, int NL, int MINB, int C>
 __global__ void __launch_bounds__(256, MINB) k_far_col_near(
     int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
     int leaf_off, const int* __restrict__ upper_start, const int* __restrict__ far_rs,
@@ -1891,7 +1905,7 @@ __global__ void __launch_bounds__(256, MINB) k_far_col_near(
   int e;
   if (warp < n_fine) {
     const int t = fine[warp];
-    far_col_body<M>(t, lane, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img, up, down, slot);
+    far_col_body<M, C>(t, lane, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img, up, down, slot);
     e = (t / npp) * epp + (t % npp - leaf_off);
   } else if (warp < n_fine + n_rest) {
     e = rest[warp - n_fine];
@@ -2390,9 +2404,13 @@ void H2Device::stage_plan() {
     sym_far_ = !stored_couplings() && d.kind() == kLaplace && m >= 2 && m <= 6;
     {
       const char* fk = std::getenv("IGB_FAR_KERNEL");
+      // column stream, two columns per lane (c5: 14.57 -> 11.0 ms per matvec,
+      // c2: 0.379 -> 0.348 ms against the lane-tile kernel)
       far_col_ = sym_far_ && m <= 5 && Lp.world == 1 && !(fk && std::strcmp(fk, "tile") == 0);
       const char* fm = std::getenv("IGB_FAR_COL_MINB");
-      far_col_minb_ = fm ? std::atoi(fm) : 3;
+      far_col_minb_ = fm ? std::atoi(fm) : 2;
+      const char* fc = std::getenv("IGB_FAR_COL_C");
+      far_col_c_ = fc ? std::atoi(fc) : 2;
     }
     // other kinds / larger m, one GPU: the warp-row symmetric kernel
     sym_w_ = !stored_couplings() && !sym_far_ && Lp.world == 1 && mm >= 32 && mm <= 128;
@@ -2819,6 +2837,10 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
     ++launches;
   }
   mark(5);
+  if (far_only_) {  // introspection: stop after the far field (phase 4)
+    if (pev == nullptr) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+    return;
+  }
   if (pev != nullptr) {  // profiling: the near rows serialised as their own phase
     k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s>>>(
         nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
@@ -2914,17 +2936,19 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
     if (n == 0) return;
     const unsigned g = grid_for(static_cast<long long>(n) * 32, 256);
     if (far_col_ && m <= 5) {
+#define IGB_FC(M_, MB_, C_) k_far_col<M_, MB_, C_><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_)
       switch (m) {
-        case 2: k_far_col<2, 4><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-        case 3: k_far_col<3, 4><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-        case 4: k_far_col<4, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        case 2: IGB_FC(2, 4, 1); break;
+        case 3: IGB_FC(3, 4, 1); break;
+        case 4: if (far_col_c_ == 2) IGB_FC(4, 3, 2); else IGB_FC(4, 3, 1); break;
         default:
-          if (far_col_minb_ == 2)
-            k_far_col<5, 2><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
-          else
-            k_far_col<5, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
+          if (far_col_c_ == 3) IGB_FC(5, 2, 3);
+          else if (far_col_c_ == 4) IGB_FC(5, 1, 4);
+          else if (far_col_c_ == 2) { if (far_col_minb_ == 2) IGB_FC(5, 2, 2); else IGB_FC(5, 3, 2); }
+          else { if (far_col_minb_ == 2) IGB_FC(5, 2, 1); else IGB_FC(5, 3, 1); }
           break;
       }
+#undef IGB_FC
       ++launches;
       return;
     }
@@ -2954,7 +2978,7 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   tick("far_coarse");
   far_lower(side2, 2);
   tick("far_lower_coarse");
-  for (int l = 0; l + 1 < L; ++l) {
+  for (int l = 0; l + 1 < L && !far_only_; ++l) {
     const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
     launch_down_level<S>(grid_for(tot, 256), side2, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
                          d_tl_, d_tr_, down, Lp.c0, Lp.c1);
@@ -2973,12 +2997,22 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
             reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
             reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
       };
-      if (far_col_ && m == 4)
-        fused_launch(k_far_col_near<4, NL, 3>);
-      else if (far_col_ && far_col_minb_ == 2)
-        fused_launch(k_far_col_near<5, NL, 2>);
-      else if (far_col_)
-        fused_launch(k_far_col_near<5, NL, 3>);
+      if (far_col_ && m == 4) {
+        if (far_col_c_ == 2) fused_launch(k_far_col_near<4, NL, 3, 2>);
+        else fused_launch(k_far_col_near<4, NL, 3, 1>);
+      } else if (far_col_) {
+        if (far_col_c_ == 3) {
+          fused_launch(k_far_col_near<5, NL, 2, 3>);
+        } else if (far_col_c_ == 4) {
+          fused_launch(k_far_col_near<5, NL, 1, 4>);
+        } else if (far_col_c_ == 2) {
+          if (far_col_minb_ == 2) fused_launch(k_far_col_near<5, NL, 2, 2>);
+          else fused_launch(k_far_col_near<5, NL, 3, 2>);
+        } else {
+          if (far_col_minb_ == 2) fused_launch(k_far_col_near<5, NL, 2, 1>);
+          else fused_launch(k_far_col_near<5, NL, 3, 1>);
+        }
+      }
       else if (m == 4)
         fused_launch(k_far_sym_near<4, NL, IGB_M4_MINB>);
       else
@@ -2992,6 +3026,10 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   far_lower(s, 1);
   tick("far_lower_leaf");
   if (!prof) IGB_CUDA(cudaStreamWaitEvent(s, ev_join2_, 0));
+  if (far_only_) {  // introspection: stop after the far field (phase 4)
+    if (!prof) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+    return;
+  }
   {
     const int l = L - 1;
     const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
@@ -3148,6 +3186,31 @@ void H2Device::profile_apply(int iters, double* phase_ms) {
     }
   }
   for (auto& e : ev) cudaEventDestroy(e);
+}
+
+void H2Device::far_field(const double* x, double* up_out, double* down_out) {
+  if (lp_.world > 1) throw std::logic_error("far_field: not available on a rank of a distributed operator");
+  IGB_CUDA(cudaSetDevice(device_));
+  const size_t sw = is_complex() ? 16 : 8;
+  IGB_CUDA(cudaDeviceSynchronize());
+  IGB_CUDA(cudaMemcpy(dx_, x, static_cast<size_t>(dim()) * sw, cudaMemcpyHostToDevice));
+  far_only_ = true;
+  try {
+    if (split_graph())
+      dispatch_kind([&](auto kt) {
+        if constexpr (decltype(kt)::KIND == 0) enqueue_apply_split<decltype(kt)>(dx_, dy_, stream_);
+      });
+    else
+      enqueue_apply_dispatch(dx_, dy_, stream_, nullptr);
+  } catch (...) {
+    far_only_ = false;
+    throw;
+  }
+  far_only_ = false;
+  IGB_CUDA(cudaStreamSynchronize(stream_));
+  const size_t n = static_cast<size_t>(plan_.n_nodes) * nch_ * plan_.m * plan_.m * sw;
+  if (up_out) IGB_CUDA(cudaMemcpy(up_out, d_up_, n, cudaMemcpyDeviceToHost));
+  if (down_out) IGB_CUDA(cudaMemcpy(down_out, d_down_, n, cudaMemcpyDeviceToHost));
 }
 
 std::vector<std::pair<std::string, double>> H2Device::profile_kernels(int iters) {

@@ -70,6 +70,9 @@ class H2Device {
   // the level-split matvec graph's kernels launched one after another on the
   // handle's stream, each timed with CUDA events: (name, ms summed over iters)
   std::vector<std::pair<std::string, double>> profile_kernels(int iters);
+  // matvec phases 1-4 on host x (through the far field and its slot sums):
+  // up and down ([node][c*m^2 + nu], Scalar) to host
+  void far_field(const double* x, double* up_out, double* down_out);
   // unordered far pairs the symmetric far kernels evaluate: [leaf level, above]
   long long sym_pairs(int which) const { return sym_pairs_[which]; }
   // `steps` x (device assembly + `matvecs` matvecs), CUDA events; returns ms
@@ -145,7 +148,8 @@ class H2Device {
   bool sym_far_ = false;  // Laplace m <= 6: lane-tile symmetric far kernel
   bool sym_w_ = false;    // other kinds / m, one GPU: warp-row symmetric far kernel
   bool far_col_ = false;  // Laplace m <= 5, one GPU: column-stream far kernel (k_far_col)
-  int far_col_minb_ = 3;
+  int far_col_minb_ = 2, far_col_c_ = 2;
+  bool far_only_ = false;  // far_field(): enqueue only phases 1-4
   int n_sym_targets_ = 0;
   int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;
   int n_sym_fine_ = 0, n_sym_coarse_ = 0;  // leaf-level / coarser symmetric targets

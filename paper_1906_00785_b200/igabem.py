@@ -91,7 +91,7 @@ SYMBOLS = (
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_create_ex", "igb_plan_counts", "igb_plan_near_pairs",
     "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
     "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
-    "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work",
+    "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work", "igb_h2_far_field",
 )
 
 
@@ -172,6 +172,7 @@ def lib():
     L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
     L.igb_release_device_memory.argtypes = [i32]
     L.igb_h2_far_work.argtypes = [vp, P(i64)]
+    L.igb_h2_far_field.argtypes = [vp, P(f64), P(f64), P(f64)]
     L.igb_h2_profile_kernels.argtypes = [vp, i32, i32, ctypes.c_char_p, P(f64), P(i32)]
     _LIB = L
     return L
@@ -588,6 +589,19 @@ class H2Matrix:
             key = names.raw[32 * k:32 * (k + 1)].split(b"\0")[0].decode()
             out[key] = out.get(key, 0.0) + float(ms[k])
         return out
+
+    def far_field(self, x):
+        """(up, down) after the far field of a matvec on x (phase 4 of apply,
+        h2.cpp:312-326), each (node_count, nch * m^2): the far-field kernel's own
+        output, for parity checks against the oracle."""
+        x = np.ascontiguousarray(x, dtype=self.dtype)
+        if x.shape != (self.rows(),):
+            raise ValueError("H2Matrix::far_field: dimension mismatch")
+        shp = (self.node_count, self.nch * self.opts.m ** 2)
+        up, down = np.zeros(shp, dtype=self.dtype), np.zeros(shp, dtype=self.dtype)
+        _check(lib().igb_h2_far_field(self._h, _p(x.view(np.float64)), _p(up.view(np.float64)),
+                                      _p(down.view(np.float64))))
+        return up, down
 
     def far_sym_counts(self):
         """unordered far pairs evaluated per matvec by the symmetric far kernels:

@@ -8,8 +8,10 @@ import numpy as np
 import pytest
 
 GOLD = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
-SMALL = [g for g in GOLD if not os.path.basename(g).startswith("c2_")]
-BIG = [g for g in GOLD if os.path.basename(g).startswith("c2_")]
+# full-size fixtures (c2, c4): only the B200 side runs them (the oracle's own
+# c4 operator stores 34 GB of couplings; tests/test_gpu_full_size.py probes it)
+BIG = [g for g in GOLD if os.path.basename(g).startswith(("c2_", "c4_"))]
+SMALL = [g for g in GOLD if g not in BIG]
 
 
 def load(path):

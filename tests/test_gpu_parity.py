@@ -99,6 +99,40 @@ def test_matvec(built, case, stored):
     assert np.array_equal(h.apply(x), y)
 
 
+def _node_rel(got, ref):
+    """worst per-node relative error (nodes below 1e-6 of the largest are
+    measured against that floor)"""
+    mag = np.abs(ref).max(axis=1)
+    floor = 1e-6 * mag.max()
+    return float((np.abs(got - ref).max(axis=1) / np.maximum(mag, floor)).max())
+
+
+@pytest.mark.parametrize("variant", ["default", "stored", "tile"])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
+def test_far_field_per_node(built, igb, case, variant, monkeypatch):
+    """The far-field kernel's own output: up (phase 3) and down after the far
+    field and its transposed-slot sums (phase 4, h2.cpp:312-326) per cluster
+    node against the oracle -- catches an error in the on-the-fly couplings
+    (the Newton-refined rsqrt, the shifted dot-form distances) or in the slot
+    bookkeeping that the aggregate matvec norm could hide."""
+    if variant == "tile":  # the lane-tile symmetric kernel (multi-GPU ranks, m = 6)
+        monkeypatch.setenv("IGB_FAR_KERNEL", "tile")
+        d = igb.Discretization(igb.make_sphere(), _pde(igb, case[0]), *case[1:4])
+        h = igb.H2Matrix(d, igb.H2Options(m=case[4], eta=1.6))
+        _, _, od, oh = built(*case)
+    else:
+        d, h, od, oh = built(*case, stored=variant == "stored")
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, d.dof_count())
+    if h.dtype == np.complex128:
+        x = x + 1j * rng.uniform(-1, 1, d.dof_count())
+    up, down = h.far_field(x)
+    _, up_r, d4_r, _ = oh.apply_ex(x)
+    assert _node_rel(up, up_r) < TOL
+    assert _node_rel(down, d4_r) < TOL
+    assert np.linalg.norm(down - d4_r) / np.linalg.norm(d4_r) < TOL
+
+
 def test_linearity(built):
     d, h, _, _ = built("laplace", 0, 1, 2, 4)
     rng = np.random.default_rng(1)

@@ -4,6 +4,7 @@ igabem core compiled against the Eigen-subset shim).  Run in this container
 
     python tools/make_golden.py            # small cases
     python tools/make_golden.py c2         # full-size c2 matvec (minutes)
+    python tools/make_golden.py c4         # full-size c4 (Maxwell, 34 GB of couplings in host RAM)
 
 Each fixture stores the configuration, the seeded input x
 (uniform[-1,1], numpy default_rng(20261019)), y = H x, partition counts,
@@ -29,6 +30,7 @@ SMALL = {
     "maxwell_P2_L2_m8_k2pi": ("maxwell", 2, 1, 2, 8, 2 * np.pi),
 }
 BIG = {"c2_laplace_P3_L6_m4": ("laplace", 3, 1, 6, 4, 0.0)}
+BIG_C4 = {"c4_maxwell_P2_L5_m8_k2pi": ("maxwell", 2, 1, 5, 8, 2 * np.pi)}
 
 
 def make(name, cfg, nblocks=400):
@@ -54,6 +56,7 @@ def make(name, cfg, nblocks=400):
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = BIG if len(sys.argv) > 1 and sys.argv[1] == "c2" else SMALL
+    arg = sys.argv[1] if len(sys.argv) > 1 else ""
+    which = {"c2": BIG, "c4": BIG_C4}.get(arg, SMALL)
     for name, cfg in which.items():
         make(name, cfg)
