@@ -100,9 +100,12 @@ typedef struct {
  * CUDA device `device`.  The discretization may be destroyed afterwards. */
 int igb_h2_create(const igb_discretization* d, const igb_h2_opts* opts, int device, igb_h2** out);
 /* flags for igb_h2_create_ex: IGB_H2_STORED_COUPLINGS keeps the far couplings
- * in HBM in the reference format (h2.cpp:218-229); the default evaluates them
- * on the fly inside the matvec (same values, no coupling storage) */
-enum { IGB_H2_STORED_COUPLINGS = 2, IGB_H2_DEVICE_PARTITION = 4 };
+ * in HBM in the reference format (h2.cpp:218-229) and streams them in every
+ * matvec; IGB_H2_FUSED_COUPLINGS evaluates them on the fly inside the matvec
+ * (same values, no coupling storage).  Neither: Laplace evaluates on the fly,
+ * Helmholtz / Maxwell store when the couplings fit in half the free device
+ * memory (igb_h2_create always chooses this way). */
+enum { IGB_H2_STORED_COUPLINGS = 2, IGB_H2_DEVICE_PARTITION = 4, IGB_H2_FUSED_COUPLINGS = 8 };
 int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, igb_h2** out);
 /* ---- multi-GPU row-cluster partition ----
  * rank `rank` of `world` assembles and applies the block rows of its level-1

@@ -1188,6 +1188,70 @@ __global__ void __launch_bounds__(256) k_far(int n_targets, const int* __restric
   }
 }
 
+// Stored-coupling far field, one CTA per target (h2.cpp:312-326): its 8 warps
+// take the target's pairs round-robin (each streams a pair's m^2 x m^2 block
+// with lanes on rows nu, 8 coupling loads in flight per lane), and the warps'
+// partial sums are added in fixed warp order through shared memory.  Balances
+// targets with ~190 pairs against those with a few (the warp-per-target
+// kernel left c4 at 49 % of HBM).
+template <class S, int NCH, int R>
+__global__ void __launch_bounds__(256, 2) k_far_cta(const int* __restrict__ targets, const int* __restrict__ far_rs,
+                                                 const int* __restrict__ far_b, const S* __restrict__ K, int mm,
+                                                 const S* __restrict__ up, S dw, S* __restrict__ down) {
+  extern __shared__ __align__(16) double far_cta_sh[];
+  S* part_sh = reinterpret_cast<S*>(far_cta_sh);  // [warp][c * mm + nu]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = targets[blockIdx.x];
+  const int rows = NCH * mm;
+  S acc[NCH][R];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[c][r] = zero<S>();
+  const int q1 = far_rs[t + 1];
+  constexpr int B = 16 / R;  // coupling columns loaded per batch: 16 loads in flight per lane
+  for (int q = far_rs[t] + w; q < q1; q += 8) {
+    const S* Kq = K + static_cast<size_t>(q) * mm * mm;
+    const S* src = up + static_cast<size_t>(__ldg(far_b + q)) * rows;
+    for (int mu0 = 0; mu0 < mm; mu0 += B) {
+      S kv[B][R];
+#pragma unroll
+      for (int j = 0; j < B; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int nu = lane + 32 * r, mu = mu0 + j;
+          kv[j][r] = (nu < mm && mu < mm) ? ldg_s(Kq + static_cast<size_t>(mu) * mm + nu) : zero<S>();
+        }
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        if (mu0 + j >= mm) break;
+        S xv[NCH];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) xv[c] = ldg_s(src + c * mm + mu0 + j);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) fmac(acc[c][r], kv[j][r], xv[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int nu = lane + 32 * r;
+    if (nu < mm)
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) part_sh[static_cast<size_t>(w) * rows + c * mm + nu] = acc[c][r];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    S v = part_sh[i];
+#pragma unroll
+    for (int ww = 1; ww < 8; ++ww) v = v + part_sh[static_cast<size_t>(ww) * rows + i];
+    if (NCH == 4 && i >= 3 * mm) v = v * dw;  // divergence channel weight -kappa^-2
+    down[static_cast<size_t>(t) * rows + i] = v;
+  }
+}
+
 // Fused far field: couplings evaluated on the fly from the L2-resident node
 // images, K_q[nu][mu] = G(|img_t[nu] - img_s[mu]|) (h2.cpp:218-229), applied
 // as in h2.cpp:312-326.  One warp per target; G lane groups take alternate
@@ -1728,6 +1792,119 @@ __global__ void __launch_bounds__(256, MINB) k_far_col(int n_targets, const int*
                      up, down, slot);
 }
 
+// Column-stream far field with the target's rows split over a warp PAIR
+// (rows [0, H) and [H, m^2), H = ceil(m^2 / 2)): half the row accumulators per
+// thread (m = 5: 16 instead of 32 registers of acc), so twice the resident
+// warps hide the FP64 / MUFU latencies.  Both warps stream the same columns;
+// the upper half's column sums K^T up[t] go through shared memory (double
+// buffered, one named barrier per chunk) and the lower half adds them in fixed
+// order (rows [0, H) + rows [H, m^2)) before writing the slot.
+template <int M, int C>
+__device__ __forceinline__ void far_col2_body(int t, int half, int lane, int pair_in_cta, double* __restrict__ sh,
+                                              double* __restrict__ xbuf, const int* __restrict__ upper_start,
+                                              const int* __restrict__ far_rs, const int* __restrict__ far_b,
+                                              const int* __restrict__ trans, const double* __restrict__ img,
+                                              const double* __restrict__ up, double* __restrict__ down,
+                                              double* __restrict__ slot) {
+  constexpr int MM = M * M, H = (MM + 1) / 2, R = ColRows<H>::R;
+  const int r0 = half * H;
+  // my rows: sh[4 i .. 4 i + 3] = (-2 t', |t'|^2), sh[4 H + i] = up[t][r0 + i]; a
+  // missing last row (odd m^2) is padded far away with zero weight
+  const double* ti = img + static_cast<size_t>(t) * MM * 3;
+  const double cx = __ldg(ti), cy = __ldg(ti + 1), cz = __ldg(ti + 2);
+  for (int i = lane; i < H; i += 32) {
+    const int nu = r0 + i;
+    double* r = sh + 4 * i;
+    if (nu < MM) {
+      const double x = __ldg(ti + 3 * nu) - cx, y = __ldg(ti + 3 * nu + 1) - cy, z = __ldg(ti + 3 * nu + 2) - cz;
+      r[0] = -2.0 * x;
+      r[1] = -2.0 * y;
+      r[2] = -2.0 * z;
+      r[3] = x * x + y * y + z * z;
+      sh[4 * H + i] = __ldg(up + static_cast<size_t>(t) * MM + nu);
+    } else {
+      r[0] = r[1] = r[2] = 0.0;
+      r[3] = 1.0e16;
+      sh[4 * H + i] = 0.0;
+    }
+  }
+  __syncwarp();
+  double acc[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) acc[i] = 0.0;
+  const int q0 = upper_start[t];
+  const int ncol = (far_rs[t + 1] - q0) * MM;
+  int buf = 0;
+  for (int c0 = 0; c0 < ncol; c0 += 32 * C, buf ^= 1) {
+    double sx[C], sy[C], sz[C], xs[C], ns[C], ps[C];
+    int q[C], mu[C];
+    bool ok[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const int c = c0 + 32 * k + lane;
+      ok[k] = c < ncol;
+      const int qi = ok[k] ? c / MM : 0;
+      mu[k] = ok[k] ? c - qi * MM : 0;
+      q[k] = q0 + qi;
+      const int s = ok[k] ? __ldg(far_b + q[k]) : t;
+      const double* p = img + (static_cast<size_t>(s) * MM + mu[k]) * 3;
+      sx[k] = __ldg(p) - cx;
+      sy[k] = __ldg(p + 1) - cy;
+      sz[k] = __ldg(p + 2) - cz;
+      xs[k] = __ldg(up + static_cast<size_t>(s) * MM + mu[k]);
+      if (!ok[k]) {
+        sx[k] = 1.0e8;
+        sy[k] = sz[k] = 0.0;
+        xs[k] = 0.0;
+      }
+      ns[k] = sx[k] * sx[k] + sy[k] * sy[k] + sz[k] * sz[k];
+      ps[k] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double2 a01 = *reinterpret_cast<const double2*>(sh + 4 * i);
+      const double2 a23 = *reinterpret_cast<const double2*>(sh + 4 * i + 2);
+      const double xt = sh[4 * H + i];
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const double r2 = fma(a01.x, sx[k], fma(a01.y, sy[k], fma(a23.x, sz[k], a23.y + ns[k])));
+        const double gk = far_rsqrt(r2);
+        acc[i] = fma(gk, xs[k], acc[i]);
+        ps[k] = fma(gk, xt, ps[k]);
+      }
+    }
+    double* xb = xbuf + buf * 32 * C;
+    if (half == 1) {
+#pragma unroll
+      for (int k = 0; k < C; ++k) xb[32 * k + lane] = ps[k];
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair_in_cta) : "memory");
+    if (half == 0) {
+#pragma unroll
+      for (int k = 0; k < C; ++k)
+        if (ok[k]) slot[static_cast<size_t>(__ldg(trans + q[k])) * MM + mu[k]] = (ps[k] + xb[32 * k + lane]) * kFarScale;
+    }
+  }
+  col_reduce_rows<H>(acc, lane);
+  if (lane < H && r0 + lane < MM) down[static_cast<size_t>(t) * MM + r0 + lane] = acc[0] * kFarScale;
+}
+
+template <int M, int MINB, int C>
+__global__ void __launch_bounds__(256, MINB) k_far_col2(int n_targets, const int* __restrict__ targets,
+                                                       const int* __restrict__ upper_start,
+                                                       const int* __restrict__ far_rs, const int* __restrict__ far_b,
+                                                       const int* __restrict__ trans, const double* __restrict__ img,
+                                                       const double* __restrict__ up, double* __restrict__ down,
+                                                       double* __restrict__ slot) {
+  constexpr int H = (M * M + 1) / 2;
+  __shared__ __align__(16) double sh[8][5 * H + (5 * H) % 2];
+  __shared__ __align__(16) double xbuf[4][2 * 32 * C];
+  const int w = threadIdx.x >> 5, pair = (blockIdx.x * blockDim.x + threadIdx.x) >> 6;
+  if (pair >= n_targets) return;  // warp-pair uniform: both warps of a pair leave together
+  far_col2_body<M, C>(targets[pair], w & 1, threadIdx.x & 31, w >> 1, sh[w], xbuf[w >> 1], upper_start, far_rs,
+                      far_b, trans, img, up, down, slot);
+}
+
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
 // in ascending t (fixed order)
 // Unconditional, unrolled stream over the row's contiguous slots.  Multi-GPU:
@@ -1913,6 +2090,38 @@ __global__ void __launch_bounds__(256, MINB) k_far_col_near(
     return;
   }
   near_row<double, NL, true>(e, lane, near_rs, near_b, blk, x, rows_out, l2g, sg);
+}
+
+// Leaf-level pair-split column-stream far field fused with the near rows: pair
+// p < n_fine evaluates leaf target fine[p]; then its lower warp streams that
+// leaf's element's near row and its upper warp the row of rest[p]; the rest
+// elements beyond n_fine take both warps of the extra pairs.
+template <int M, int NL, int MINB, int C>
+__global__ void __launch_bounds__(256, MINB) k_far_col2_near(
+    int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
+    int leaf_off, const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+    const int* __restrict__ far_b, const int* __restrict__ trans, const double* __restrict__ img,
+    const double* __restrict__ up, double* __restrict__ down, double* __restrict__ slot,
+    const unsigned char* __restrict__ /*owned: single GPU*/, const int* __restrict__ near_rs,
+    const int* __restrict__ near_b, const double* __restrict__ blk, const double* __restrict__ x,
+    double* __restrict__ rows_out, const int* __restrict__ l2g, const double* __restrict__ sg) {
+  constexpr int H = (M * M + 1) / 2;
+  __shared__ __align__(16) double sh[8][5 * H + (5 * H) % 2];
+  __shared__ __align__(16) double xbuf[4][2 * 32 * C];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, half = w & 1;
+  const int pair = (blockIdx.x * blockDim.x + threadIdx.x) >> 6;
+  int e = -1;
+  if (pair < n_fine) {
+    const int t = fine[pair];
+    far_col2_body<M, C>(t, half, lane, w >> 1, sh[w], xbuf[w >> 1], upper_start, far_rs, far_b, trans, img, up,
+                        down, slot);
+    if (half == 0) e = (t / npp) * epp + (t % npp - leaf_off);
+    else if (pair < n_rest) e = rest[pair];
+  } else {
+    const int r = n_fine + 2 * (pair - n_fine) + half;
+    if (r < n_rest) e = rest[r];
+  }
+  if (e >= 0) near_row<double, NL, true>(e, lane, near_rs, near_b, blk, x, rows_out, l2g, sg);
 }
 
 // leaf backward transform moments^T down + near rows (h2.cpp:359-371); one
@@ -2131,7 +2340,10 @@ H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, i
                    int device, int flags, int world, int rank)
     : disc_(std::move(d)), device_(device), flags_(flags) {
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("H2Matrix: bad rank/world");
-  if (world > 1 && (flags & 2)) throw std::invalid_argument("H2Matrix: stored couplings are single-GPU only");
+  if (world > 1 && (flags & kStoredCouplings))
+    throw std::invalid_argument("H2Matrix: stored couplings are single-GPU only");
+  if ((flags & kStoredCouplings) && (flags & kFusedCouplings))
+    throw std::invalid_argument("H2Matrix: stored and on-the-fly couplings requested together");
   const auto t_wall0 = std::chrono::steady_clock::now();
   check_h2_options(*disc_, m, eta, far_order, sing_order, &nfar_, &nsing_);
   if (nsing_ > 16) throw std::invalid_argument("B200 H2: singular order > 16 not supported (32-bit point index)");
@@ -2219,6 +2431,17 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   lp_ = build_local_plan(d, plan_, opt_.world, opt_.rank);
   times_.plan_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   lap("plan");
+  // couplings stored or evaluated in every matvec: unless forced, complex kinds
+  // store them when they fit in half the free device memory -- their m^4
+  // complex kernel evaluations per pair cost more than streaming the block
+  // (c4: 6.2 ms per matvec stored at 93 % of HBM vs 14.6 ms evaluated); Laplace
+  // always evaluates them (c5: the symmetric FP64 kernel beats the 161 GB stream)
+  if (!(flags_ & (kStoredCouplings | kFusedCouplings)) && opt_.world == 1 && d.is_complex()) {
+    size_t free_b = 0, total_b = 0;
+    IGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t mm = static_cast<size_t>(opt_.m) * opt_.m;
+    if (plan_.far_a.size() * mm * mm * 16 <= free_b / 2) flags_ |= kStoredCouplings;
+  }
   for (int c = 1; c <= 3; ++c) {  // topology items == the near list's singular pairs
     const SingList &T = sing_items_[c], &L = lp_.sing[c];
     if (T.ea != L.ea || T.eb != L.eb || T.map_a != L.map_a || T.map_b != L.map_b)
@@ -2270,6 +2493,8 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   IGB_CUDA(cudaEventCreateWithFlags(&ev_apply_done_, cudaEventDisableTiming));
   IGB_CUDA(cudaEventRecord(ev_apply_done_, stream_));
   IGB_CUDA(cudaMemsetAsync(d_up_, 0, nn * rows * sw * 8, stream_));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_cta<typename KT::S, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  IGB_CUDA(cudaFuncSetAttribute(k_far_cta<typename KT::S, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   IGB_CUDA(cudaFuncSetAttribute(k_far_fused<KT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -2753,7 +2978,19 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
         dw = mk(w.real(), w.imag());
       }
       const S* K = reinterpret_cast<const S*>(d_far_);
-      if (nch_ == 4) {
+      if (mm >= 32) {  // one CTA per target
+        const size_t smem = static_cast<size_t>(8) * nch_ * mm * sizeof(S);
+        const unsigned nt = static_cast<unsigned>(n_far_targets_);
+        if (nch_ == 4) {
+          if (mm <= 32) k_far_cta<S, 4, 1><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else if (mm <= 64) k_far_cta<S, 4, 2><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else k_far_cta<S, 4, 4><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        } else {
+          if (mm <= 32) k_far_cta<S, 1, 1><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else if (mm <= 64) k_far_cta<S, 1, 2><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else k_far_cta<S, 1, 4><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        }
+      } else if (nch_ == 4) {
         if (mm <= 32) k_far<S, 4, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
         else if (mm <= 64) k_far<S, 4, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
         else k_far<S, 4, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
@@ -2942,7 +3179,9 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
         case 3: IGB_FC(3, 4, 1); break;
         case 4: if (far_col_c_ == 2) IGB_FC(4, 3, 2); else IGB_FC(4, 3, 1); break;
         default:
-          if (far_col_c_ == 3) IGB_FC(5, 2, 3);
+          if (far_col_c_ == 12) k_far_col2<5, 3, 2><<<grid_for(static_cast<long long>(n) * 64, 256), 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
+          else if (far_col_c_ == 11) k_far_col2<5, 3, 1><<<grid_for(static_cast<long long>(n) * 64, 256), 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
+          else if (far_col_c_ == 3) IGB_FC(5, 2, 3);
           else if (far_col_c_ == 4) IGB_FC(5, 1, 4);
           else if (far_col_c_ == 2) { if (far_col_minb_ == 2) IGB_FC(5, 2, 2); else IGB_FC(5, 3, 2); }
           else { if (far_col_minb_ == 2) IGB_FC(5, 2, 1); else IGB_FC(5, 3, 1); }
@@ -3001,7 +3240,15 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
         if (far_col_c_ == 2) fused_launch(k_far_col_near<4, NL, 3, 2>);
         else fused_launch(k_far_col_near<4, NL, 3, 1>);
       } else if (far_col_) {
-        if (far_col_c_ == 3) {
+        if (far_col_c_ == 12 || far_col_c_ == 11) {
+          const long long pairs = static_cast<long long>(n_sym_fine_) + std::max(0, (n_near_rest_ - n_sym_fine_ + 1) / 2);
+          auto k2 = far_col_c_ == 12 ? k_far_col2_near<5, NL, 3, 2> : k_far_col2_near<5, NL, 3, 1>;
+          k2<<<grid_for(pairs * 64, 256), 256, 0, s>>>(
+              n_sym_fine_, d_sym_fine_, n_near_rest_, d_near_rest_, epp, npp, P.level_offset[L], d_upper_start_,
+              d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, d_near_rs_, d_near_b_,
+              reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
+              reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
+        } else if (far_col_c_ == 3) {
           fused_launch(k_far_col_near<5, NL, 2, 3>);
         } else if (far_col_c_ == 4) {
           fused_launch(k_far_col_near<5, NL, 1, 4>);

@@ -25,7 +25,9 @@ struct DeviceBytes {
 class H2Device {
  public:
   // flags bit1 (IGB_H2_STORED_COUPLINGS): store the far couplings (reference
-  // format) instead of evaluating them inside the matvec
+  // format) instead of evaluating them inside the matvec; bit3
+  // (IGB_H2_FUSED_COUPLINGS): always evaluate them; neither: chosen per kind
+  // and size after the block partition
   // world > 1: this rank assembles and applies the block rows of its level-1
   // clusters (build_local_plan); apply via dist_phase1 / all-gather /
   // dist_phase2 / all-reduce
@@ -36,7 +38,8 @@ class H2Device {
   H2Device& operator=(const H2Device&) = delete;
 
   const Discretization& disc() const { return *disc_; }
-  bool stored_couplings() const { return (flags_ & 2) != 0; }
+  enum { kStoredCouplings = 2, kDevicePartition = 4, kFusedCouplings = 8 };  // include/igabem_b200.h flags
+  bool stored_couplings() const { return (flags_ & kStoredCouplings) != 0; }
   const H2Plan& plan() const { return plan_; }
   const LocalPlan& local_plan() const { return lp_; }
   // multi-GPU matvec: phase 1 (x -> packed owned up moments, `send` holds

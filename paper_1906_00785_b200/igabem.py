@@ -440,18 +440,20 @@ class H2Matrix:
     complex128 for Helmholtz / Maxwell), like the reference's Eigen vectors."""
 
     def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int = 0,
-                 stored_couplings: bool = False, world: int = 1, rank: int = 0, device_partition: bool = False):
+                 stored_couplings: bool | None = None, world: int = 1, rank: int = 0,
+                 device_partition: bool = False):
         opts = opts or H2Options()
         o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
         h = ctypes.c_void_p()
-        flags = (2 if stored_couplings else 0) | (4 if device_partition else 0)
+        # stored_couplings: True -> stream stored couplings, False -> evaluate them
+        # in every matvec, None -> chosen per kind and size (include/igabem_b200.h)
+        flags = {True: 2, False: 8, None: 0}[stored_couplings] | (4 if device_partition else 0)
         if world == 1:
             _check(lib().igb_h2_create_ex(disc._h, ctypes.byref(o), int(device), flags, ctypes.byref(h)))
         else:
             _check(lib().igb_h2_create_dist(disc._h, ctypes.byref(o), int(device), flags, int(world), int(rank),
                                             ctypes.byref(h)))
         self.world, self.rank, self.device = world, rank, device
-        self.stored_couplings = stored_couplings
         self._h = h
         self._disc = disc
         self.opts = opts
@@ -470,6 +472,11 @@ class H2Matrix:
         return self._disc.dof_count()
 
     cols = rows
+
+    @property
+    def stored_couplings(self):
+        """whether this operator streams stored couplings (else evaluates them per matvec)"""
+        return self.device_bytes()["far"] > 0
 
     def apply(self, x):
         x = np.ascontiguousarray(x, dtype=self.dtype)
