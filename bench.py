@@ -396,9 +396,10 @@ def run_b200(args, c, name):
     launches = args.steps * (n_asm_k + mv * n_mv_k)
     # -- e2e through the public API with host buffers: H2Matrix(disc) (host
     # plan + uploads + kernels) + mv x apply(host x) (H2D x, graph, D2H y)
-    x_host = np.random.default_rng(20261019).uniform(-1, 1, N)
-    if h.dtype == np.complex128:
-        x_host = x_host + 0j
+    # x and y in page-locked host memory (the contract's pinned host buffers)
+    tdt = torch.complex128 if h.dtype == np.complex128 else torch.float64
+    x_host = torch.from_numpy(np.random.default_rng(20261019).uniform(-1, 1, N)).to(tdt).pin_memory().numpy()
+    y_host = torch.empty(N, dtype=tdt).pin_memory().numpy()
     upload = h.upload_bytes()
     del h
     e2e_times = []
@@ -407,7 +408,7 @@ def run_b200(args, c, name):
         t0 = time.perf_counter()
         he = igb.H2Matrix(disc, opts, device=dev)
         for _ in range(mv):
-            y = he.apply(x_host)
+            y = he.apply(x_host, out=y_host)
         _ = float(y[0].real)
         dt = time.perf_counter() - t0
         if it > 0:

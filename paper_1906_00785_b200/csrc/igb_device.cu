@@ -3518,21 +3518,38 @@ void H2Device::apply_device(const double* x, double* y, cudaStream_t s) {
   IGB_CUDA(cudaEventRecord(ev_apply_done_, s));
 }
 
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 void H2Device::apply_host(const double* x, double* y) {
   const size_t bytes = static_cast<size_t>(dim()) * (is_complex() ? 16 : 8);
   IGB_CUDA(cudaSetDevice(device_));
-  if (!h_x_pinned_) {
+  // page-locked caller buffers are copied directly; pageable ones go through
+  // the handle's pinned staging buffers
+  const bool px = is_pinned(x), py = is_pinned(y);
+  if (!h_x_pinned_ && !(px && py)) {
     h_x_pinned_ = static_cast<double*>(pinned_get(bytes));
     h_y_pinned_ = static_cast<double*>(pinned_get(bytes));
   }
-  std::memcpy(h_x_pinned_, x, bytes);
+  const double* xs = x;
+  if (!px) {
+    std::memcpy(h_x_pinned_, x, bytes);
+    xs = h_x_pinned_;
+  }
+  double* ys = py ? y : h_y_pinned_;
   IGB_CUDA(cudaStreamWaitEvent(stream_, ev_apply_done_, 0));  // a device apply on another stream
-  IGB_CUDA(cudaMemcpyAsync(dx_, h_x_pinned_, bytes, cudaMemcpyHostToDevice, stream_));
+  IGB_CUDA(cudaMemcpyAsync(dx_, xs, bytes, cudaMemcpyHostToDevice, stream_));
   launch_apply_graph(stream_);
-  IGB_CUDA(cudaMemcpyAsync(h_y_pinned_, dy_, bytes, cudaMemcpyDeviceToHost, stream_));
+  IGB_CUDA(cudaMemcpyAsync(ys, dy_, bytes, cudaMemcpyDeviceToHost, stream_));
   IGB_CUDA(cudaEventRecord(ev_apply_done_, stream_));
   IGB_CUDA(cudaStreamSynchronize(stream_));
-  std::memcpy(y, h_y_pinned_, bytes);
+  if (!py) std::memcpy(y, h_y_pinned_, bytes);
 }
 
 void H2Device::near_blocks(long long first, long long count, double* out) const {

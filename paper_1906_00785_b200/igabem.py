@@ -478,11 +478,18 @@ class H2Matrix:
         """whether this operator streams stored couplings (else evaluates them per matvec)"""
         return self.device_bytes()["far"] > 0
 
-    def apply(self, x):
+    def apply(self, x, out=None):
+        """y = H x on host vectors; `out` (optional) receives y.  Page-locked
+        buffers (e.g. torch pin_memory().numpy()) are transferred directly."""
         x = np.ascontiguousarray(x, dtype=self.dtype)
         if x.shape != (self.rows(),):
             raise ValueError("H2Matrix::apply: dimension mismatch")
-        y = np.empty_like(x)
+        if out is None:
+            y = np.empty_like(x)
+        else:
+            y = out
+            if y.shape != x.shape or y.dtype != x.dtype or not y.flags.c_contiguous:
+                raise ValueError("H2Matrix::apply: out must be a contiguous vector like x")
         _check(lib().igb_h2_apply(self._h, _p(x.view(np.float64)), _p(y.view(np.float64))))
         return y
 
@@ -670,13 +677,27 @@ class DistH2Matrix:
         return self.h.rows()
 
     def apply(self, x, y=None):
+        """y = H x with x, y replicated device tensors.  NCCL: the collectives run
+        on the device tensors on torch's current stream; any other backend
+        (gloo: CPU-only process groups, tests) stages them through host memory."""
         torch = self.torch
         y = torch.empty_like(x) if y is None else y
         stream = torch.cuda.current_stream().cuda_stream
         self.h.dist_phase1(x.data_ptr(), self.send.data_ptr(), stream)
-        self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        nccl = self.dist.get_backend(self.group) == "nccl"
+        if nccl:
+            self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        else:
+            parts = [torch.empty(self.send.numel(), dtype=self.dtype) for _ in range(self.world)]
+            self.dist.all_gather(parts, self.send.cpu(), group=self.group)
+            self.recv.copy_(torch.cat(parts))
         self.h.dist_phase2(self.recv.data_ptr(), y.data_ptr(), torch.cuda.current_stream().cuda_stream)
-        self.dist.all_reduce(y, group=self.group)
+        if nccl:
+            self.dist.all_reduce(y, group=self.group)
+        else:
+            yh = y.cpu()
+            self.dist.all_reduce(yh, group=self.group)
+            y.copy_(yh)
         return y
 
 

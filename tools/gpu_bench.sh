@@ -1,7 +1,8 @@
 #!/bin/bash
-# default bench run (as the driver runs it) + smoke
-mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
-cat gpurun_out/smoke.log; tail -2 gpurun_out/bench.log | cut -c1-600; tail -2 gpurun_out/bench_ref.log | cut -c1-900
+# default bench (c5) + a short reference arm; outputs in gpurun_out/
+cd "$GRAFT_REPO_ROOT"
+tag=${1:-r02}
+timeout 1500 python bench.py ${BENCH_ARGS:-} > gpurun_out/${tag}_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/${tag}_bench.log
+if [ -n "$WITH_REF" ]; then
+  timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${tag}_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/${tag}_ref.log
+fi
