@@ -116,6 +116,9 @@ int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int d
 int igb_h2_create_dist(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, int world,
                        int rank, igb_h2** out);
 int igb_h2_dist_send_count(const igb_h2* h, size_t* scalars);
+/* mask[dof] = 1 where this rank's block rows (elements) contribute to y[dof];
+ * DOFs set on several ranks are the cut DOFs the y reduction must sum */
+int igb_h2_dist_dof_mask(const igb_h2* h, unsigned char* mask);
 int igb_h2_dist_phase1(igb_h2* h, const double* x, double* send, void* stream);
 int igb_h2_dist_phase2(igb_h2* h, const double* recv, double* y_partial, void* stream);
 /* rows()/cols()  h2.hpp:62-63 */

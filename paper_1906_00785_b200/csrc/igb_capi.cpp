@@ -223,6 +223,14 @@ int igb_h2_dist_send_count(const igb_h2* h, size_t* scalars) {
     *scalars = h->dev->send_count();
   });
 }
+int igb_h2_dist_dof_mask(const igb_h2* h, unsigned char* mask) {
+  return guard([&] {
+    need(h, "h2");
+    need(mask, "mask");
+    const auto& ds = h->dev->local_plan().dof_start;
+    for (size_t i = 0; i + 1 < ds.size(); ++i) mask[i] = ds[i + 1] > ds[i] ? 1 : 0;
+  });
+}
 int igb_h2_dist_phase1(igb_h2* h, const double* x, double* send, void* stream) {
   return guard([&] {
     need(h, "h2");

@@ -1705,12 +1705,18 @@ __device__ __forceinline__ void col_reduce_rows(double (&acc)[ColRows<MM>::R], i
   }
 }
 
-template <int M, int C>
+// LIST (multi-GPU ranks): the target's columns come from an explicit pair list
+// (col_q[col_rs[w] ..]): q >= 0 a pair with an owned source s > t (symmetric:
+// the transposed product goes to the slot of (s, t)), ~q a pair whose source
+// is another rank's node (one-sided: no slot; that rank evaluates its own side)
+template <int M, int C, bool LIST = false>
 __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict__ sh,
                                              const int* __restrict__ upper_start, const int* __restrict__ far_rs,
                                              const int* __restrict__ far_b, const int* __restrict__ trans,
                                              const double* __restrict__ img, const double* __restrict__ up,
-                                             double* __restrict__ down, double* __restrict__ slot) {
+                                             double* __restrict__ down, double* __restrict__ slot,
+                                             const int* __restrict__ col_q = nullptr, int col_q0 = 0,
+                                             int col_q1 = 0) {
   constexpr int MM = M * M, R = ColRows<MM>::R;
   // target rows: sh[4 nu .. 4 nu + 3] = (-2 t'x, -2 t'y, -2 t'z, |t'|^2) (two
   // 16 B broadcasts), sh[4 MM + nu] = up[t][nu]
@@ -1729,20 +1735,27 @@ __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict
   double acc[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) acc[i] = 0.0;
-  const int q0 = upper_start[t];
-  const int ncol = (far_rs[t + 1] - q0) * MM;
+  const int q0 = LIST ? col_q0 : upper_start[t];
+  const int ncol = ((LIST ? col_q1 : far_rs[t + 1]) - q0) * MM;
   // C columns per lane: each broadcast target row feeds C evaluations
   for (int c0 = 0; c0 < ncol; c0 += 32 * C) {
     double sx[C], sy[C], sz[C], xs[C], ns[C], ps[C];
     int q[C], mu[C];
-    bool ok[C];
+    bool ok[C], sym[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       const int c = c0 + 32 * k + lane;
       ok[k] = c < ncol;
       const int qi = ok[k] ? c / MM : 0;
       mu[k] = ok[k] ? c - qi * MM : 0;
-      q[k] = q0 + qi;
+      if constexpr (LIST) {
+        const int qe = ok[k] ? __ldg(col_q + q0 + qi) : 0;
+        sym[k] = qe >= 0;
+        q[k] = qe >= 0 ? qe : ~qe;
+      } else {
+        sym[k] = true;
+        q[k] = q0 + qi;
+      }
       const int s = ok[k] ? __ldg(far_b + q[k]) : t;
       const double* p = img + (static_cast<size_t>(s) * MM + mu[k]) * 3;
       sx[k] = __ldg(p) - cx;
@@ -1772,7 +1785,7 @@ __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict
     }
 #pragma unroll
     for (int k = 0; k < C; ++k)
-      if (ok[k]) slot[static_cast<size_t>(__ldg(trans + q[k])) * MM + mu[k]] = ps[k] * kFarScale;
+      if (ok[k] && sym[k]) slot[static_cast<size_t>(__ldg(trans + q[k])) * MM + mu[k]] = ps[k] * kFarScale;
   }
   col_reduce_rows<MM>(acc, lane);
   if (lane < MM) down[static_cast<size_t>(t) * MM + lane] = acc[0] * kFarScale;
@@ -1790,6 +1803,19 @@ __global__ void __launch_bounds__(256, MINB) k_far_col(int n_targets, const int*
   if (warp >= n_targets) return;
   far_col_body<M, C>(targets[warp], threadIdx.x & 31, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img,
                      up, down, slot);
+}
+
+template <int M, int MINB, int C>
+__global__ void __launch_bounds__(256, MINB) k_far_col_list(int n_targets, const int* __restrict__ targets,
+                                                           const int* __restrict__ col_rs, const int* __restrict__ col_q,
+                                                           const int* __restrict__ far_b, const int* __restrict__ trans,
+                                                           const double* __restrict__ img, const double* __restrict__ up,
+                                                           double* __restrict__ down, double* __restrict__ slot) {
+  __shared__ __align__(16) double sh[8][(5 * M * M + 1) / 2 * 2];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= n_targets) return;
+  far_col_body<M, C, true>(targets[warp], threadIdx.x & 31, sh[threadIdx.x >> 5], nullptr, nullptr, far_b, trans, img,
+                           up, down, slot, col_q, col_rs[warp], col_rs[warp + 1]);
 }
 
 // Column-stream far field with the target's rows split over a warp PAIR
@@ -2681,6 +2707,19 @@ void H2Device::stage_plan() {
         n_near_rest_ = static_cast<int>(rest.size());
         d_near_rest_ = upload(rest);
       }
+      if (Lp.world > 1 && sym_far_ && m <= 5) {  // per-target column lists for k_far_col_list
+        std::vector<int> col_rs(1, 0), col_q;
+        for (int t : sym_targets) {
+          for (int q = P.far_row_start[t]; q < P.far_row_start[t + 1]; ++q) {
+            const int sq = P.far_b[q];
+            if (!Lp.node_owned[sq]) col_q.push_back(~q);
+            else if (sq > t) col_q.push_back(q);
+          }
+          col_rs.push_back(static_cast<int>(col_q.size()));
+        }
+        d_col_rs_ = upload(col_rs);
+        d_col_q_ = upload(col_q);
+      }
       d_upper_start_ = upload(P.far_upper_start);
       d_trans_ = upload(P.far_trans);
       const size_t per_pair = static_cast<size_t>(mm) * (sym_w_ ? static_cast<size_t>(nch_) * sw : 1);
@@ -3011,6 +3050,18 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
     k_far_sym<MM_, false, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,        \
                                                  d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, \
                                                  d_owned_, lp_.world > 1 ? 1 : 0)
+      if (lp_.world > 1 && m <= 5 && d_col_q_) {  // column stream over the rank's pair lists
+#define IGB_FCL(M_, MB_, C_)                                                                                 \
+  k_far_col_list<M_, MB_, C_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_col_rs_, d_col_q_, d_far_b_, \
+                                                   d_trans_, d_img_, upd, dn, d_slot_)
+        switch (m) {
+          case 2: IGB_FCL(2, 4, 1); break;
+          case 3: IGB_FCL(3, 4, 1); break;
+          case 4: IGB_FCL(4, 3, 2); break;
+          default: IGB_FCL(5, 2, 2); break;
+        }
+#undef IGB_FCL
+      } else
       switch (m) {  // occupancy chosen so no variant spills (ptxas -warn-spills)
         case 2: IGB_FS(2, 3); break;
         case 3: IGB_FS(3, 3); break;

@@ -155,6 +155,7 @@ class H2Device {
   bool far_only_ = false;  // far_field(): enqueue only phases 1-4
   int n_sym_targets_ = 0;
   int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;
+  int *d_col_rs_ = nullptr, *d_col_q_ = nullptr;  // multi-GPU ranks: per-target pair lists (k_far_col_list)
   int n_sym_fine_ = 0, n_sym_coarse_ = 0;  // leaf-level / coarser symmetric targets
   long long sym_pairs_[2] = {0, 0};        // unordered far pairs evaluated by them
   int *d_sym_fine_ = nullptr, *d_sym_coarse_ = nullptr;

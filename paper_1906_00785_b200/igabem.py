@@ -91,7 +91,7 @@ SYMBOLS = (
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_create_ex", "igb_plan_counts", "igb_plan_near_pairs",
     "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
     "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
-    "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work", "igb_h2_far_field",
+    "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work", "igb_h2_far_field", "igb_h2_dist_dof_mask",
 )
 
 
@@ -172,6 +172,7 @@ def lib():
     L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
     L.igb_release_device_memory.argtypes = [i32]
     L.igb_h2_far_work.argtypes = [vp, P(i64)]
+    L.igb_h2_dist_dof_mask.argtypes = [vp, P(ctypes.c_ubyte)]
     L.igb_h2_far_field.argtypes = [vp, P(f64), P(f64), P(f64)]
     L.igb_h2_profile_kernels.argtypes = [vp, i32, i32, ctypes.c_char_p, P(f64), P(i32)]
     _LIB = L
@@ -507,6 +508,12 @@ class H2Matrix:
         _check(lib().igb_h2_dist_send_count(self._h, ctypes.byref(n)))
         return n.value
 
+    def dist_dof_mask(self):
+        """bool per DOF: this rank's block rows contribute to y there"""
+        m = np.zeros(self.rows(), dtype=np.uint8)
+        _check(lib().igb_h2_dist_dof_mask(self._h, _p(m, ctypes.c_ubyte)))
+        return m.astype(bool)
+
     def dist_phase1(self, x_ptr, send_ptr, stream=0):
         _check(lib().igb_h2_dist_phase1(self._h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(send_ptr),
                                         ctypes.c_void_p(stream or None)))
@@ -669,9 +676,30 @@ class DistH2Matrix:
         self.h = H2Matrix(disc, opts, device=dev, world=self.world, rank=self.rank)
         self.dtype = torch.complex128 if self.h.dtype == np.complex128 else torch.float64
         n = self.h.dist_send_count()
-        self.send = torch.zeros(max(n, 1), dtype=self.dtype, device=f"cuda:{dev}")
-        self.recv = torch.zeros(max(n, 1) * self.world, dtype=self.dtype, device=f"cuda:{dev}")
+        dv = f"cuda:{dev}"
+        self.send = torch.zeros(max(n, 1), dtype=self.dtype, device=dv)
+        self.recv = torch.zeros(max(n, 1) * self.world, dtype=self.dtype, device=dv)
         self.n = n
+        # y reduction over the cut DOFs only: masks of all ranks (once); a DOF
+        # touched by several ranks is cut and summed by an all-reduce over the
+        # compact cut list; every DOF is owned by the lowest rank touching it,
+        # whose values all ranks all-gather to replicate y
+        mine = torch.from_numpy(self.h.dist_dof_mask().astype(np.uint8))
+        masks = [torch.zeros_like(mine) for _ in range(self.world)]
+        self._gather_cpu_or_dev(masks, mine, dev)
+        M = np.stack([m.numpy().astype(bool) for m in masks])
+        touched = M.sum(axis=0)
+        owner = np.argmax(M, axis=0)  # lowest touching rank (untouched DOFs: rank 0, value 0)
+        self.cut = torch.from_numpy(np.flatnonzero(touched > 1)).to(dv)
+        own = [np.flatnonzero(owner == r) for r in range(self.world)]
+        self.own_max = max(len(o) for o in own)
+        self.own_idx = [torch.from_numpy(o).to(dv) for o in own]
+        self.cut_buf = torch.zeros(max(len(self.cut), 1), dtype=self.dtype, device=dv)
+        self.own_buf = torch.zeros(self.own_max, dtype=self.dtype, device=dv)
+        self.all_buf = torch.zeros(self.own_max * self.world, dtype=self.dtype, device=dv)
+        oth = [(own[r], r * self.own_max + np.arange(len(own[r]))) for r in range(self.world) if r != self.rank]
+        self.other_idx = torch.from_numpy(np.concatenate([o[0] for o in oth] or [np.zeros(0, np.int64)])).to(dv)
+        self.other_pos = torch.from_numpy(np.concatenate([o[1] for o in oth] or [np.zeros(0, np.int64)])).to(dv)
 
     def rows(self):
         return self.h.rows()
@@ -692,13 +720,39 @@ class DistH2Matrix:
             self.dist.all_gather(parts, self.send.cpu(), group=self.group)
             self.recv.copy_(torch.cat(parts))
         self.h.dist_phase2(self.recv.data_ptr(), y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        # cut DOFs: sum the partial values (fixed rank order in NCCL's / gloo's
+        # reduction); then replicate y from the owners
+        if len(self.cut):
+            torch.index_select(y, 0, self.cut, out=self.cut_buf)
+            self._allreduce(self.cut_buf)
+            y.index_copy_(0, self.cut, self.cut_buf)
+        mine = self.own_idx[self.rank]
+        self.own_buf[:len(mine)] = y[mine]
         if nccl:
-            self.dist.all_reduce(y, group=self.group)
+            self.dist.all_gather_into_tensor(self.all_buf, self.own_buf, group=self.group)
         else:
-            yh = y.cpu()
-            self.dist.all_reduce(yh, group=self.group)
-            y.copy_(yh)
+            parts = [torch.empty(self.own_max, dtype=self.dtype) for _ in range(self.world)]
+            self.dist.all_gather(parts, self.own_buf.cpu(), group=self.group)
+            self.all_buf.copy_(torch.cat(parts))
+        y.index_copy_(0, self.other_idx, self.all_buf[self.other_pos])
         return y
+
+    def _allreduce(self, t):
+        if self.dist.get_backend(self.group) == "nccl":
+            self.dist.all_reduce(t, group=self.group)
+        else:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+
+    def _gather_cpu_or_dev(self, outs, t, dev):
+        if self.dist.get_backend(self.group) == "nccl":
+            o = [x.to(f"cuda:{dev}") for x in outs]
+            self.dist.all_gather(o, t.to(f"cuda:{dev}"), group=self.group)
+            for a, b in zip(outs, o):
+                a.copy_(b.cpu())
+        else:
+            self.dist.all_gather(outs, t, group=self.group)
 
 
 # ----------------------------------------------------------- SURVEY 8(f)
