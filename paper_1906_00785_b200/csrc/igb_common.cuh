@@ -201,9 +201,6 @@ __device__ __forceinline__ typename KT::S green_k(double r2, const KParams& kp) 
   else
     return green_c(r2, kp);
 }
-#ifndef IGB_GREEN_FAR
-#define IGB_GREEN_FAR green_far  // A/B: -DIGB_GREEN_FAR=green_k
-#endif
 
 // -------------------------------------------------------- geometry jet
 // cf: [c][j][i] (stride 5 / 25), homogeneous (wx, wy, wz, w) in (s, t)

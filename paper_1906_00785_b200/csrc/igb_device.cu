@@ -331,9 +331,6 @@ __global__ void k_dense_rows(int n_rows, const int* __restrict__ rows, int nd, c
 // (ea <= eb) writing the compact block, which k_sing_scatter places in the
 // two ordered slots (pair_integration.hpp:139-148).
 
-#ifndef IGB_SING_VEC
-#define IGB_SING_VEC 1
-#endif
 // Sum-factorised geometry jet.  Setup (once per rule line, element, homogeneous
 // component): with the fixed cell coordinate f, A_o = sum_k c[o][k] f^k and
 // B_o its derivative in f (the inner Horner loops of jet<4>); for a moving v
@@ -357,14 +354,9 @@ __device__ __forceinline__ void jet_setup(const double* __restrict__ comp, int v
                                           double* __restrict__ out) {
   double res[10];
   jet_setup_regs(comp, v_moves, f, res);
-#if IGB_SING_VEC
   double2* o2 = reinterpret_cast<double2*>(out);
 #pragma unroll
   for (int k = 0; k < 5; ++k) o2[k] = make_double2(res[2 * k], res[2 * k + 1]);
-#else
-#pragma unroll
-  for (int k = 0; k < 10; ++k) out[k] = res[k];
-#endif
 }
 // One homogeneous component at the moving coordinate y: the outer Horner loop
 // of jet<4> (the same arithmetic when v moves) -> value and the two partials.
@@ -398,7 +390,6 @@ __device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_mo
   double N[4], Ns[4], Nt[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-#if IGB_SING_VEC
     // 16 B shared loads (st is 16 B aligned): half the load instructions
     double A[10];
     const double2* A2 = reinterpret_cast<const double2*>(st + c * 10);
@@ -408,22 +399,10 @@ __device__ __forceinline__ void jet_line(const double* __restrict__ st, int v_mo
       A[2 * k] = v.x;
       A[2 * k + 1] = v.y;
     }
-#else
-    const double* A = st + c * 10;
-#endif
     jet_comp(A, v_moves, y, N[c], Ns[c], Nt[c]);
   }
   jet_quot(N, Ns, Nt, x, du, dv);
 }
-#ifndef IGB_VERTEX_FIXED
-#define IGB_VERTEX_FIXED 1
-#endif
-#ifndef IGB_EDGE_I3
-#define IGB_EDGE_I3 1
-#endif
-#ifndef IGB_RANK1
-#define IGB_RANK1 1
-#endif
 // Vertex lines fix both parameters of element a: its setup tasks finish the
 // component's jet at the fixed point ([N, Ns, Nt, -] per component) and the
 // points only form the quotient.
@@ -431,17 +410,11 @@ __device__ __forceinline__ void jet_fixed(const double* __restrict__ st, double 
   double N[4], Ns[4], Nt[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-#if IGB_SING_VEC
     const double2* A2 = reinterpret_cast<const double2*>(st + c * 10);
     const double2 a = A2[0], b = A2[1];
     N[c] = a.x;
     Ns[c] = a.y;
     Nt[c] = b.x;
-#else
-    N[c] = st[c * 10];
-    Ns[c] = st[c * 10 + 1];
-    Nt[c] = st[c * 10 + 2];
-#endif
   }
   jet_quot(N, Ns, Nt, x, du, dv);
 }
@@ -499,7 +472,6 @@ __device__ __forceinline__ void rule_line(int line, int n, float rn, const doubl
   } else if constexpr (CLS == 2) {  // edge (quadrature.cpp:113-149)
     const int kind = sec >> 1;
     const double sgn = (sec & 1) ? -1.0 : 1.0;
-#if IGB_EDGE_I3
     // lines run over i3 (the decoded innermost index is i4): the element whose
     // point does not depend on i3 (a for kinds 0 and 2, b for kind 1) is fixed
     // along the line, the other moves its v (t * gx[i3])
@@ -527,23 +499,6 @@ __device__ __forceinline__ void rule_line(int line, int n, float rn, const doubl
     }
     wl = w3 * jac;
     (void)i1;
-#else
-    const double t = gx[i1], a = gx[i2], b = gx[i3];
-    double d, jac, va, vb;
-    if (kind == 0) {
-      va = t; vb = t * b; d = sgn * t * a; jac = t * t * (1.0 - t * a);
-    } else if (kind == 1) {
-      vb = t; va = t * b; d = sgn * t * a; jac = t * t * (1.0 - t * a);
-    } else {
-      d = sgn * t; va = t * a; vb = t * b; jac = t * t * (1.0 - t);
-    }
-    const double u0 = fmax(0.0, -d), ul = 1.0 - fabs(d);
-    c0[0] = u0;     c1[0] = ul;
-    c0[1] = va;     c1[1] = 0.0;
-    c0[2] = u0 + d; c1[2] = ul;
-    c0[3] = vb;     c1[3] = 0.0;
-    wl = w3 * jac;
-#endif
   } else {  // vertex (quadrature.cpp:151-177)
     const double t = gx[i1];
     const double v1 = t * gx[i2], v2 = t * gx[i3];
@@ -577,12 +532,7 @@ struct SingArgs {
   double* out;  // compact blocks [item][la][lb] (scattered by k_sing_scatter)
 };
 
-#ifndef IGB_SING_LMAX
-#define IGB_SING_LMAX 16  // 8 setup tasks per line: one round of 128 threads
-#endif
-#ifndef IGB_SING_NTH96
-#define IGB_SING_NTH96 1
-#endif
+constexpr int kSingLmax = 16; // 8 setup tasks per line: one round of 128 threads
 // NTH threads per CTA: 128, or 96 when a chunk holds <= 96 points (n = 6: 16
 // lines x 6), so no warp idles through the point phase and 5 CTAs fit an SM
 template <class KT, int NTH = 128>
@@ -594,41 +544,27 @@ struct SingLayout {
   static constexpr int HEAD = 104 * 2 + 2 * KT::TABN + 128;
   static constexpr int STAGE = CH * STR * (SW + 1);
   static constexpr int RED = SL * NL * NL * SW;
-  static constexpr int R1 = CH * STR * SW + 2 * IGB_SING_LMAX * (NL + 1) + 2 * IGB_SING_LMAX * NL * SW;  // rank-1 path
+  static constexpr int R1 = CH * STR * SW + 2 * kSingLmax * (NL + 1) + 2 * kSingLmax * NL * SW;  // rank-1 path
   static constexpr int BODY0 = STAGE > RED ? STAGE : RED;
   static constexpr int BODY1 = (KT::KIND != 2 && R1 > BODY0) ? R1 : BODY0;
   static constexpr int BODY = (BODY1 + 1) & ~1;  // keeps the setup lines 16 B aligned
-  static constexpr int LMAX = IGB_SING_LMAX;    // rule lines per chunk (setup capacity)
+  static constexpr int LMAX = kSingLmax;    // rule lines per chunk (setup capacity)
   // real kernels with up to 9 local functions fit 128 registers: 4 CTAs / SM
-#ifndef IGB_SING_MINB
-#define IGB_SING_MINB 4
-#endif
-#ifndef IGB_SING_MINB16
-#define IGB_SING_MINB16 4
-#endif
-#ifndef IGB_SING_MINBM
-#define IGB_SING_MINBM 1
-#endif
-#ifndef IGB_SING_MINBH
-#define IGB_SING_MINBH 4
-#endif
-#ifndef IGB_SING_MINB96
-#define IGB_SING_MINB96 5
-#endif
-  static constexpr int MINB = (NTH == 96)                     ? (NL <= 9 && KT::KIND != 2 ? IGB_SING_MINB96 : 1)
-                              : (KT::KIND == 0 && NL <= 9)    ? IGB_SING_MINB
-                              : (KT::KIND == 0 && NL <= 16) ? IGB_SING_MINB16
-                              : (KT::KIND == 1 && NL <= 9)  ? IGB_SING_MINBH
-                              : (KT::KIND == 2 && NL <= 12) ? IGB_SING_MINBM
+  static constexpr int kSingMinb = 4;
+  static constexpr int kSingMinb16 = 4;
+  static constexpr int kSingMinbM = 1;
+  static constexpr int kSingMinbH = 4;
+  static constexpr int kSingMinb96 = 5;
+  static constexpr int MINB = (NTH == 96)                     ? (NL <= 9 && KT::KIND != 2 ? kSingMinb96 : 1)
+                              : (KT::KIND == 0 && NL <= 9)    ? kSingMinb
+                              : (KT::KIND == 0 && NL <= 16) ? kSingMinb16
+                              : (KT::KIND == 1 && NL <= 9)  ? kSingMinbH
+                              : (KT::KIND == 2 && NL <= 12) ? kSingMinbM
                                                             : 1;
   // per line: [element][component][A0..4, B0..4] (80), the affine rule
   // descriptor (c0, c1) x 4 + weight (9); odd stride (the lines of one warp
   // read distinct banks)
-#if IGB_SING_VEC
   static constexpr int LSTRIDE = 2 * 4 * 10 + 10;  // even: 16 B aligned lines (20-bank offset per line)
-#else
-  static constexpr int LSTRIDE = 2 * 4 * 10 + 9;
-#endif
   static constexpr int SETUP = LMAX * LSTRIDE;
   static constexpr size_t BYTES = static_cast<size_t>(HEAD + BODY + SETUP) * 8;
   static_assert(NL % TS == 0, "tile");
@@ -639,9 +575,9 @@ struct SingLayout {
 // real q = 2 +1..2 %, so real kernels keep 128 threads)
 template <class KT>
 constexpr bool sing96_ok() {
-  return IGB_SING_NTH96 && KT::KIND == 1 && KT::NL <= 9;
+  return KT::KIND == 1 && KT::NL <= 9;
 }
-inline bool sing96_use(int n) { return (IGB_SING_LMAX < 128 / n ? IGB_SING_LMAX : 128 / n) * n <= 96; }
+inline bool sing96_use(int n) { return (kSingLmax < 128 / n ? kSingLmax : 128 / n) * n <= 96; }
 
 template <class KT, int CLS, int NTH = 128>
 __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(GeoArgs g, SingArgs A) {
@@ -691,13 +627,13 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
   // is C + C^T (the Galerkin symmetry the reference tests, test_assembly.cpp:20-29)
   const bool half = CLS == 3 && ma == mb;
   // an element fixed along every rule line: vertex (a), edge with lines over i3
-  constexpr bool kFixedEl = (IGB_VERTEX_FIXED && CLS == 1) || (IGB_EDGE_I3 && CLS == 2);
+  constexpr bool kFixedEl = CLS == 1 || CLS == 2;
   // scalar shapes with a fixed element: the line's contribution is rank one,
   // s_fixed (x) sum_k gwt_k s_moving,k (or its transpose), so the points stage
   // gwt s_moving only and the block takes one outer product per line
   // (measured: P = 4 edge -12 %, vertex -21 %; Helmholtz q = 2 -1..-3 %; real
   // q = 2 (nl = 9) +2..4 %, where the point-wise GEMM is only ~23 % of the time)
-  constexpr bool kRank1 = kFixedEl && KT::KIND != 2 && NC == 1 && IGB_RANK1 && (NL >= 16 || KT::KIND == 1);
+  constexpr bool kRank1 = kFixedEl && KT::KIND != 2 && NC == 1 && (NL >= 16 || KT::KIND == 1);
   const int npts = (CLS == 3 ? (half ? 4 : 8) : (CLS == 2 ? 6 : 4)) * n4;
 
   S acc[TS][TS];
@@ -758,12 +694,7 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
         if (e == 0 && c == 0) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-#if IGB_SING_VEC
             reinterpret_cast<double2*>(L + 80)[k] = make_double2(c0[k], c1[k]);
-#else
-            L[80 + 2 * k] = c0[k];
-            L[81 + 2 * k] = c1[k];
-#endif
           }
           L[88] = wl;
         }
@@ -819,28 +750,17 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
       if (p < npts) {
         const double* L = setup + my_ll * LY::LSTRIDE;
         const double gk4 = gx[my_k];
-#if IGB_SING_VEC
         const double2* D = reinterpret_cast<const double2*>(L + 80);
         const double2 du_ = D[0], dv_ = D[1], dub_ = D[2], dvb_ = D[3];
         const double ua = fma(du_.y, gk4, du_.x), va = fma(dv_.y, gk4, dv_.x);
         const double ub = fma(dub_.y, gk4, dub_.x), vb = fma(dvb_.y, gk4, dvb_.x);
         const int vma = dv_.y != 0.0, vmb = dvb_.y != 0.0;
-#else
-        const double ua = fma(L[81], gk4, L[80]), va = fma(L[83], gk4, L[82]);
-        const double ub = fma(L[85], gk4, L[84]), vb = fma(L[87], gk4, L[86]);
-        const int vma = L[83] != 0.0, vmb = L[87] != 0.0;
-#endif
         const double w = L[88] * gw[my_k];
         const double sa_ = sxa + h * ua, ta_ = sya + h * va, sb_ = sxb + h * ub, tb_ = syb + h * vb;
         double xa[3], dua[3], dva[3], xb[3], dub[3], dvb[3];
         // vertex: a always fixed, b never; edge: per line (kind 1 fixes b)
-#if IGB_SING_VEC
         const bool fa = kFixedEl && (CLS == 1 || (du_.y == 0.0 && dv_.y == 0.0));
         const bool fbx = kFixedEl && CLS != 1 && dub_.y == 0.0 && dvb_.y == 0.0;
-#else
-        const bool fa = kFixedEl && (CLS == 1 || (L[81] == 0.0 && L[83] == 0.0));
-        const bool fbx = kFixedEl && CLS != 1 && L[85] == 0.0 && L[87] == 0.0;
-#endif
         if constexpr (kFixedEl) {
           if (fa)
             jet_fixed(L, xa, dua, dva);
@@ -1328,7 +1248,7 @@ __global__ void __launch_bounds__(256) k_far_fused(int n_targets, const int* __r
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const double d0 = tx[r][0] - xy.x, d1 = tx[r][1] - xy.y, d2 = tx[r][2] - sz;
-          const S gk = IGB_GREEN_FAR<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+          const S gk = green_far<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
 #pragma unroll
           for (int c = 0; c < NCH; ++c) fmac(part[c][r], gk, xv[c]);
         }
@@ -1445,7 +1365,7 @@ __global__ void __launch_bounds__(256) k_far_sym_w(int n_targets, const int* __r
       for (int r = 0; r < R; ++r) {
         if (lane + 32 * r >= mm) continue;
         const double d0 = tx[r][0] - xy.x, d1 = tx[r][1] - xy.y, d2 = tx[r][2] - sz;
-        const S gk = IGB_GREEN_FAR<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
+        const S gk = green_far<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           fmac(acc[c][r], gk, xs[c]);
@@ -1481,39 +1401,13 @@ __global__ void __launch_bounds__(256) k_far_sym_w(int n_targets, const int* __r
 
 
 template <int M>
-struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair
+struct SymTile {  // lane grid BR x BC over the (nu, mu) block of one far pair (m = 6)
   static constexpr int MM = M * M;
-  // m = 4: 4 x 8 lanes (A/B on B200: 0.37 ms vs 0.41 ms for 2 x 16 at c2);
-  // m = 5: 5 x 6 lanes, an exact 5 x 5 tile each (30 of 32 lanes)
-#ifndef IGB_LEAF_DOWN_V2
-#define IGB_LEAF_DOWN_V2 1
-#endif
-#ifndef IGB_FUSED_NEAR
-#define IGB_FUSED_NEAR 1  // single GPU, m = 4: leaf far field and near rows in one kernel
-#endif
-#ifndef IGB_FAR_IDX_AHEAD
-#define IGB_FAR_IDX_AHEAD 1
-#endif
-#ifndef IGB_M4_MINB
-#define IGB_M4_MINB 3
-#endif
-#ifndef IGB_M5_MINB
-#define IGB_M5_MINB 2
-#endif
-#ifndef IGB_M5_BR
-#define IGB_M5_BR 5
-#define IGB_M5_BC 6
-#endif
-  static constexpr int BR = (M == 5) ? IGB_M5_BR : (M == 3 ? 3 : 4);
-  static constexpr int BC = (M == 5) ? IGB_M5_BC : (M == 2 ? 4 : (M == 3 ? 9 : 8));
+  static constexpr int BR = 4, BC = 8;
   static constexpr int RN = (MM + BR - 1) / BR, CN = (MM + BC - 1) / BC;
   static_assert(BR * BC <= 32, "lane grid");
 };
 
-#ifndef IGB_FAR_NEWTON
-#define IGB_FAR_NEWTON 1
-#endif
-#if IGB_FAR_NEWTON
 // 2/r from the MUFU estimate y0 and one Newton step y0 (3 - x y0^2) (the
 // factor 1/2 of the step folded into the final scale): relative error
 // 1.5 e0^2 for the estimate's e0
@@ -1523,10 +1417,6 @@ __device__ __forceinline__ double far_rsqrt(double x) {
   return y0 * fma(-x * y0, y0, 3.0);
 }
 constexpr double kFarScale = 0.5 * kInv4Pi;
-#else
-__device__ __forceinline__ double far_rsqrt(double x) { return rsqrt_nr(x); }
-constexpr double kFarScale = kInv4Pi;
-#endif
 
 // Symmetric fused far field (Laplace): each unordered admissible pair {t, s},
 // t < s, is evaluated once by the warp of t: K = G(|img_t[nu] - img_s[mu]|)
@@ -1567,7 +1457,7 @@ __device__ __forceinline__ void far_sym_body(int n_targets, const int* __restric
   double nsx[CN][3], nxs[CN];
   // single GPU: source indices read one pair ahead, so the image loads of pair
   // q depend on a register, not on a load issued in the same iteration
-  constexpr bool kAhead = IGB_FAR_IDX_AHEAD && !DIST;
+  constexpr bool kAhead = !DIST;
   int s_nx = (kAhead && q0 < q1) ? __ldg(far_b + q0) : 0;
   auto load = [&](int q) {
     int s;
@@ -1818,119 +1708,6 @@ __global__ void __launch_bounds__(256, MINB) k_far_col_list(int n_targets, const
                            up, down, slot, col_q, col_rs[warp], col_rs[warp + 1]);
 }
 
-// Column-stream far field with the target's rows split over a warp PAIR
-// (rows [0, H) and [H, m^2), H = ceil(m^2 / 2)): half the row accumulators per
-// thread (m = 5: 16 instead of 32 registers of acc), so twice the resident
-// warps hide the FP64 / MUFU latencies.  Both warps stream the same columns;
-// the upper half's column sums K^T up[t] go through shared memory (double
-// buffered, one named barrier per chunk) and the lower half adds them in fixed
-// order (rows [0, H) + rows [H, m^2)) before writing the slot.
-template <int M, int C>
-__device__ __forceinline__ void far_col2_body(int t, int half, int lane, int pair_in_cta, double* __restrict__ sh,
-                                              double* __restrict__ xbuf, const int* __restrict__ upper_start,
-                                              const int* __restrict__ far_rs, const int* __restrict__ far_b,
-                                              const int* __restrict__ trans, const double* __restrict__ img,
-                                              const double* __restrict__ up, double* __restrict__ down,
-                                              double* __restrict__ slot) {
-  constexpr int MM = M * M, H = (MM + 1) / 2, R = ColRows<H>::R;
-  const int r0 = half * H;
-  // my rows: sh[4 i .. 4 i + 3] = (-2 t', |t'|^2), sh[4 H + i] = up[t][r0 + i]; a
-  // missing last row (odd m^2) is padded far away with zero weight
-  const double* ti = img + static_cast<size_t>(t) * MM * 3;
-  const double cx = __ldg(ti), cy = __ldg(ti + 1), cz = __ldg(ti + 2);
-  for (int i = lane; i < H; i += 32) {
-    const int nu = r0 + i;
-    double* r = sh + 4 * i;
-    if (nu < MM) {
-      const double x = __ldg(ti + 3 * nu) - cx, y = __ldg(ti + 3 * nu + 1) - cy, z = __ldg(ti + 3 * nu + 2) - cz;
-      r[0] = -2.0 * x;
-      r[1] = -2.0 * y;
-      r[2] = -2.0 * z;
-      r[3] = x * x + y * y + z * z;
-      sh[4 * H + i] = __ldg(up + static_cast<size_t>(t) * MM + nu);
-    } else {
-      r[0] = r[1] = r[2] = 0.0;
-      r[3] = 1.0e16;
-      sh[4 * H + i] = 0.0;
-    }
-  }
-  __syncwarp();
-  double acc[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) acc[i] = 0.0;
-  const int q0 = upper_start[t];
-  const int ncol = (far_rs[t + 1] - q0) * MM;
-  int buf = 0;
-  for (int c0 = 0; c0 < ncol; c0 += 32 * C, buf ^= 1) {
-    double sx[C], sy[C], sz[C], xs[C], ns[C], ps[C];
-    int q[C], mu[C];
-    bool ok[C];
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const int c = c0 + 32 * k + lane;
-      ok[k] = c < ncol;
-      const int qi = ok[k] ? c / MM : 0;
-      mu[k] = ok[k] ? c - qi * MM : 0;
-      q[k] = q0 + qi;
-      const int s = ok[k] ? __ldg(far_b + q[k]) : t;
-      const double* p = img + (static_cast<size_t>(s) * MM + mu[k]) * 3;
-      sx[k] = __ldg(p) - cx;
-      sy[k] = __ldg(p + 1) - cy;
-      sz[k] = __ldg(p + 2) - cz;
-      xs[k] = __ldg(up + static_cast<size_t>(s) * MM + mu[k]);
-      if (!ok[k]) {
-        sx[k] = 1.0e8;
-        sy[k] = sz[k] = 0.0;
-        xs[k] = 0.0;
-      }
-      ns[k] = sx[k] * sx[k] + sy[k] * sy[k] + sz[k] * sz[k];
-      ps[k] = 0.0;
-    }
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const double2 a01 = *reinterpret_cast<const double2*>(sh + 4 * i);
-      const double2 a23 = *reinterpret_cast<const double2*>(sh + 4 * i + 2);
-      const double xt = sh[4 * H + i];
-#pragma unroll
-      for (int k = 0; k < C; ++k) {
-        const double r2 = fma(a01.x, sx[k], fma(a01.y, sy[k], fma(a23.x, sz[k], a23.y + ns[k])));
-        const double gk = far_rsqrt(r2);
-        acc[i] = fma(gk, xs[k], acc[i]);
-        ps[k] = fma(gk, xt, ps[k]);
-      }
-    }
-    double* xb = xbuf + buf * 32 * C;
-    if (half == 1) {
-#pragma unroll
-      for (int k = 0; k < C; ++k) xb[32 * k + lane] = ps[k];
-    }
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair_in_cta) : "memory");
-    if (half == 0) {
-#pragma unroll
-      for (int k = 0; k < C; ++k)
-        if (ok[k]) slot[static_cast<size_t>(__ldg(trans + q[k])) * MM + mu[k]] = (ps[k] + xb[32 * k + lane]) * kFarScale;
-    }
-  }
-  col_reduce_rows<H>(acc, lane);
-  if (lane < H && r0 + lane < MM) down[static_cast<size_t>(t) * MM + r0 + lane] = acc[0] * kFarScale;
-}
-
-template <int M, int MINB, int C>
-__global__ void __launch_bounds__(256, MINB) k_far_col2(int n_targets, const int* __restrict__ targets,
-                                                       const int* __restrict__ upper_start,
-                                                       const int* __restrict__ far_rs, const int* __restrict__ far_b,
-                                                       const int* __restrict__ trans, const double* __restrict__ img,
-                                                       const double* __restrict__ up, double* __restrict__ down,
-                                                       double* __restrict__ slot) {
-  constexpr int H = (M * M + 1) / 2;
-  __shared__ __align__(16) double sh[8][5 * H + (5 * H) % 2];
-  __shared__ __align__(16) double xbuf[4][2 * 32 * C];
-  const int w = threadIdx.x >> 5, pair = (blockIdx.x * blockDim.x + threadIdx.x) >> 6;
-  if (pair >= n_targets) return;  // warp-pair uniform: both warps of a pair leave together
-  far_col2_body<M, C>(targets[pair], w & 1, threadIdx.x & 31, w >> 1, sh[w], xbuf[w >> 1], upper_start, far_rs,
-                      far_b, trans, img, up, down, slot);
-}
-
 // down[s] += sum of the transposed contributions of the pairs (s, t), t < s,
 // in ascending t (fixed order)
 // Unconditional, unrolled stream over the row's contiguous slots.  Multi-GPU:
@@ -2062,37 +1839,9 @@ __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict
   near_row<S, NL, FROM_X>(e, threadIdx.x & 31, near_rs, near_b, blk, coef, rows_out, l2g, sg);
 }
 
-// Leaf-level far field fused with the near rows (single GPU): warp w < n_fine
-// evaluates leaf target fine[w]'s far pairs, then streams the near row of that
-// leaf's element; the remaining warps stream the rows of elements without leaf
-// far pairs.  The HBM-bound rows thus run at the tail of each warp while other
-// warps of the SM are still in the FP64-bound far loop (the separate near-row
-// kernel could not share SMs with the far field).
-template <int M, int NL, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_far_sym_near(
-    int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
-    int leaf_off, const int* __restrict__ upper_start, const int* __restrict__ far_rs,
-    const int* __restrict__ far_b, const int* __restrict__ trans, const double* __restrict__ img,
-    const double* __restrict__ up, double* __restrict__ down, double* __restrict__ slot,
-    const unsigned char* __restrict__ owned, const int* __restrict__ near_rs, const int* __restrict__ near_b,
-    const double* __restrict__ blk, const double* __restrict__ x, double* __restrict__ rows_out,
-    const int* __restrict__ l2g, const double* __restrict__ sg) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int e;
-  if (warp < n_fine) {
-    far_sym_body<M, false>(n_fine, fine, upper_start, far_rs, far_b, trans, img, up, down, slot, owned, 0);
-    const int t = fine[warp];
-    e = (t / npp) * epp + (t % npp - leaf_off);
-  } else if (warp < n_fine + n_rest) {
-    e = rest[warp - n_fine];
-  } else {
-    return;
-  }
-  near_row<double, NL, true>(e, threadIdx.x & 31, near_rs, near_b, blk, x, rows_out, l2g, sg);
-}
-
 // Leaf-level column-stream far field fused with the near rows (single GPU): as
-// k_far_sym_near, with far_col_body for the far part.
+// the HBM-bound rows run at the tail of each warp while other warps of the SM
+// are still in the FP64-bound far loop.
 template <int M, int NL, int MINB, int C>
 __global__ void __launch_bounds__(256, MINB) k_far_col_near(
     int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
@@ -2118,38 +1867,6 @@ __global__ void __launch_bounds__(256, MINB) k_far_col_near(
   near_row<double, NL, true>(e, lane, near_rs, near_b, blk, x, rows_out, l2g, sg);
 }
 
-// Leaf-level pair-split column-stream far field fused with the near rows: pair
-// p < n_fine evaluates leaf target fine[p]; then its lower warp streams that
-// leaf's element's near row and its upper warp the row of rest[p]; the rest
-// elements beyond n_fine take both warps of the extra pairs.
-template <int M, int NL, int MINB, int C>
-__global__ void __launch_bounds__(256, MINB) k_far_col2_near(
-    int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
-    int leaf_off, const int* __restrict__ upper_start, const int* __restrict__ far_rs,
-    const int* __restrict__ far_b, const int* __restrict__ trans, const double* __restrict__ img,
-    const double* __restrict__ up, double* __restrict__ down, double* __restrict__ slot,
-    const unsigned char* __restrict__ /*owned: single GPU*/, const int* __restrict__ near_rs,
-    const int* __restrict__ near_b, const double* __restrict__ blk, const double* __restrict__ x,
-    double* __restrict__ rows_out, const int* __restrict__ l2g, const double* __restrict__ sg) {
-  constexpr int H = (M * M + 1) / 2;
-  __shared__ __align__(16) double sh[8][5 * H + (5 * H) % 2];
-  __shared__ __align__(16) double xbuf[4][2 * 32 * C];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, half = w & 1;
-  const int pair = (blockIdx.x * blockDim.x + threadIdx.x) >> 6;
-  int e = -1;
-  if (pair < n_fine) {
-    const int t = fine[pair];
-    far_col2_body<M, C>(t, half, lane, w >> 1, sh[w], xbuf[w >> 1], upper_start, far_rs, far_b, trans, img, up,
-                        down, slot);
-    if (half == 0) e = (t / npp) * epp + (t % npp - leaf_off);
-    else if (pair < n_rest) e = rest[pair];
-  } else {
-    const int r = n_fine + 2 * (pair - n_fine) + half;
-    if (r < n_rest) e = rest[r];
-  }
-  if (e >= 0) near_row<double, NL, true>(e, lane, near_rs, near_b, blk, x, rows_out, l2g, sg);
-}
-
 // leaf backward transform moments^T down + near rows (h2.cpp:359-371); one
 // thread per (owned element, local function)
 template <class S, int NL>
@@ -2166,7 +1883,7 @@ __global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restri
   const S* dn = down + static_cast<size_t>(leaf) * rows;
   const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
   S acc = zero<S>();
-  if constexpr (sizeof(S) == 8 && IGB_LEAF_DOWN_V2) {
+  if constexpr (sizeof(S) == 8) {
     // rows even (m^2 nch with m even or nch = 4) and 16 B aligned: paired loads
     if ((rows & 1) == 0) {
       const double2* m2 = reinterpret_cast<const double2*>(mc);
@@ -2215,9 +1932,6 @@ using namespace dev;
 // Small, latency-bound kernels of the matvec chains are launched with
 // programmatic stream serialisation: a launch may become resident while its
 // predecessor finishes (each such kernel begins with pdl_entry()).
-#ifndef IGB_PDL
-#define IGB_PDL 1
-#endif
 template <class... KArgs, class... Args>
 static void pdl_launch(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
                        Args&&... args) {
@@ -2230,7 +1944,7 @@ static void pdl_launch(void (*kern)(KArgs...), unsigned grid, unsigned block, si
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = IGB_PDL ? 1 : 0;
+  cfg.numAttrs = 1 ? 1 : 0;
   IGB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
@@ -2653,16 +2367,10 @@ void H2Device::stage_plan() {
     d_far_targets_ = upload(targets);
     // symmetric fused far field (Laplace, m <= 6): upper pairs + transposes
     sym_far_ = !stored_couplings() && d.kind() == kLaplace && m >= 2 && m <= 6;
-    {
-      const char* fk = std::getenv("IGB_FAR_KERNEL");
-      // column stream, two columns per lane (c5: 14.57 -> 11.0 ms per matvec,
-      // c2: 0.379 -> 0.348 ms against the lane-tile kernel)
-      far_col_ = sym_far_ && m <= 5 && Lp.world == 1 && !(fk && std::strcmp(fk, "tile") == 0);
-      const char* fm = std::getenv("IGB_FAR_COL_MINB");
-      far_col_minb_ = fm ? std::atoi(fm) : 2;
-      const char* fc = std::getenv("IGB_FAR_COL_C");
-      far_col_c_ = fc ? std::atoi(fc) : 2;
-    }
+    // m <= 5, one GPU: the column-stream kernel, two columns per lane (c5:
+    // 14.57 -> 11.0 ms per matvec, c2: 0.379 -> 0.348 ms against the lane-tile
+    // kernel, which m = 6 keeps)
+    far_col_ = sym_far_ && m <= 5 && Lp.world == 1;
     // other kinds / larger m, one GPU: the warp-row symmetric kernel
     sym_w_ = !stored_couplings() && !sym_far_ && Lp.world == 1 && mm >= 32 && mm <= 128;
     if (sym_far_ || sym_w_) {
@@ -2697,7 +2405,7 @@ void H2Device::stage_plan() {
       // leaf has no upper far pairs get near-only warps
       bool ident = Lp.world == 1 && static_cast<int>(Lp.el.size()) == d.element_count();
       for (size_t i = 0; ident && i < Lp.el.size(); ++i) ident = Lp.el[i] == static_cast<int>(i);
-      if (IGB_FUSED_NEAR && sym_far_ && (m == 4 || m == 5) && ident) {
+      if (far_col_ && (m == 4 || m == 5) && ident) {
         std::vector<char> has(d.element_count(), 0);
         const int epp = d.elements_per_patch();
         for (int t : fine) has[(t / P.npp) * epp + (t % P.npp - P.level_offset[P.depth])] = 1;
@@ -3042,15 +2750,14 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
       const unsigned gsym = grid_for(static_cast<long long>(n_sym_targets_) * 32, 256);
       double* dn = reinterpret_cast<double*>(down);
       const double* upd = reinterpret_cast<const double*>(up);
-#define IGB_FS(MM_, MB_)                                                                                        \
-  if (lp_.world > 1)                                                                                           \
-    k_far_sym<MM_, true, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,       \
-                                                d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 1);     \
-  else                                                                                                         \
-    k_far_sym<MM_, false, MB_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,        \
-                                                 d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, \
-                                                 d_owned_, lp_.world > 1 ? 1 : 0)
-      if (lp_.world > 1 && m <= 5 && d_col_q_) {  // column stream over the rank's pair lists
+      if (far_col_) {  // one GPU, m <= 5 (graphs without the level split: depth 0)
+        switch (m) {
+          case 2: k_far_col<2, 4, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+          case 3: k_far_col<3, 4, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+          case 4: k_far_col<4, 3, 2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+          default: k_far_col<5, 2, 2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+        }
+      } else if (m <= 5) {  // ranks: column stream over the rank's pair lists
 #define IGB_FCL(M_, MB_, C_)                                                                                 \
   k_far_col_list<M_, MB_, C_><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_col_rs_, d_col_q_, d_far_b_, \
                                                    d_trans_, d_img_, upd, dn, d_slot_)
@@ -3061,15 +2768,13 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
           default: IGB_FCL(5, 2, 2); break;
         }
 #undef IGB_FCL
-      } else
-      switch (m) {  // occupancy chosen so no variant spills (ptxas -warn-spills)
-        case 2: IGB_FS(2, 3); break;
-        case 3: IGB_FS(3, 3); break;
-        case 4: IGB_FS(4, IGB_M4_MINB); break;
-        case 5: IGB_FS(5, IGB_M5_MINB); break;
-        default: IGB_FS(6, 1); break;
+      } else if (lp_.world > 1) {  // m = 6: the lane-tile kernel (one-sided pairs with other ranks' nodes)
+        k_far_sym<6, true, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,
+                                                   d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 1);
+      } else {
+        k_far_sym<6, false, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_,
+                                                    d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0);
       }
-#undef IGB_FS
       ++launches;
       if (lp_.world > 1)
         pdl_launch(k_far_lower<true>, grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, s, 
@@ -3223,32 +2928,20 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   auto far_sym = [&](cudaStream_t st, int n, const int* targets) {
     if (n == 0) return;
     const unsigned g = grid_for(static_cast<long long>(n) * 32, 256);
-    if (far_col_ && m <= 5) {
+    if (far_col_) {  // column stream: m <= 5
 #define IGB_FC(M_, MB_, C_) k_far_col<M_, MB_, C_><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_)
       switch (m) {
         case 2: IGB_FC(2, 4, 1); break;
         case 3: IGB_FC(3, 4, 1); break;
-        case 4: if (far_col_c_ == 2) IGB_FC(4, 3, 2); else IGB_FC(4, 3, 1); break;
-        default:
-          if (far_col_c_ == 12) k_far_col2<5, 3, 2><<<grid_for(static_cast<long long>(n) * 64, 256), 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
-          else if (far_col_c_ == 11) k_far_col2<5, 3, 1><<<grid_for(static_cast<long long>(n) * 64, 256), 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_);
-          else if (far_col_c_ == 3) IGB_FC(5, 2, 3);
-          else if (far_col_c_ == 4) IGB_FC(5, 1, 4);
-          else if (far_col_c_ == 2) { if (far_col_minb_ == 2) IGB_FC(5, 2, 2); else IGB_FC(5, 3, 2); }
-          else { if (far_col_minb_ == 2) IGB_FC(5, 2, 1); else IGB_FC(5, 3, 1); }
-          break;
+        case 4: IGB_FC(4, 3, 2); break;
+        default: IGB_FC(5, 2, 2); break;
       }
 #undef IGB_FC
       ++launches;
       return;
     }
-    switch (m) {
-      case 2: k_far_sym<2, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
-      case 3: k_far_sym<3, false, 3><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
-      case 4: k_far_sym<4, false, IGB_M4_MINB><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
-      case 5: k_far_sym<5, false, IGB_M5_MINB><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
-      default: k_far_sym<6, false, 1><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, 0); break;
-    }
+    k_far_sym<6, false, 1><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_,
+                                              upd, dn, d_slot_, d_owned_, 0);  // m = 6: lane tile
     ++launches;
   };
   auto far_lower = [&](cudaStream_t st, int which) {
@@ -3287,34 +2980,10 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
             reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
             reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
       };
-      if (far_col_ && m == 4) {
-        if (far_col_c_ == 2) fused_launch(k_far_col_near<4, NL, 3, 2>);
-        else fused_launch(k_far_col_near<4, NL, 3, 1>);
-      } else if (far_col_) {
-        if (far_col_c_ == 12 || far_col_c_ == 11) {
-          const long long pairs = static_cast<long long>(n_sym_fine_) + std::max(0, (n_near_rest_ - n_sym_fine_ + 1) / 2);
-          auto k2 = far_col_c_ == 12 ? k_far_col2_near<5, NL, 3, 2> : k_far_col2_near<5, NL, 3, 1>;
-          k2<<<grid_for(pairs * 64, 256), 256, 0, s>>>(
-              n_sym_fine_, d_sym_fine_, n_near_rest_, d_near_rest_, epp, npp, P.level_offset[L], d_upper_start_,
-              d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, d_near_rs_, d_near_b_,
-              reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
-              reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
-        } else if (far_col_c_ == 3) {
-          fused_launch(k_far_col_near<5, NL, 2, 3>);
-        } else if (far_col_c_ == 4) {
-          fused_launch(k_far_col_near<5, NL, 1, 4>);
-        } else if (far_col_c_ == 2) {
-          if (far_col_minb_ == 2) fused_launch(k_far_col_near<5, NL, 2, 2>);
-          else fused_launch(k_far_col_near<5, NL, 3, 2>);
-        } else {
-          if (far_col_minb_ == 2) fused_launch(k_far_col_near<5, NL, 2, 1>);
-          else fused_launch(k_far_col_near<5, NL, 3, 1>);
-        }
-      }
-      else if (m == 4)
-        fused_launch(k_far_sym_near<4, NL, IGB_M4_MINB>);
+      if (m == 4)
+        fused_launch(k_far_col_near<4, NL, 3, 2>);
       else
-        fused_launch(k_far_sym_near<5, NL, IGB_M5_MINB>);
+        fused_launch(k_far_col_near<5, NL, 2, 2>);
       ++launches;
     }
   } else {

@@ -151,7 +151,6 @@ class H2Device {
   bool sym_far_ = false;  // Laplace m <= 6: lane-tile symmetric far kernel
   bool sym_w_ = false;    // other kinds / m, one GPU: warp-row symmetric far kernel
   bool far_col_ = false;  // Laplace m <= 5, one GPU: column-stream far kernel (k_far_col)
-  int far_col_minb_ = 2, far_col_c_ = 2;
   bool far_only_ = false;  // far_field(): enqueue only phases 1-4
   int n_sym_targets_ = 0;
   int *d_sym_targets_ = nullptr, *d_upper_start_ = nullptr, *d_trans_ = nullptr;

@@ -7,7 +7,8 @@ import os
 import numpy as np
 import pytest
 
-GOLD = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLD = sorted(g for g in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+              if not os.path.basename(g).startswith("solve_"))  # solver fixtures: tests/test_gpu_solve.py
 # full-size fixtures (c2, c4): only the B200 side runs them (the oracle's own
 # c4 operator stores 34 GB of couplings; tests/test_gpu_full_size.py probes it)
 BIG = [g for g in GOLD if os.path.basename(g).startswith(("c2_", "c4_"))]

@@ -8,7 +8,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("laplace", 2, 1, 3, 8), ("laplace", 3, 1, 3, 4), ("laplace", 4, 1, 3, 5),
+CASES = [("laplace", 2, 1, 3, 8), ("laplace", 3, 1, 3, 4), ("laplace", 4, 1, 3, 5), ("laplace", 1, 1, 2, 6),
          ("helmholtz", 1, 1, 2, 6), ("maxwell", 2, 1, 2, 4)]
 
 

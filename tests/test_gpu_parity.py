@@ -17,6 +17,7 @@ CASES = [
     ("laplace", 3, 1, 3, 4),    # c2 space (P=3) at L=3
     ("laplace", 4, 1, 2, 5),    # c5 space (P=4) at L=2
     ("laplace", 3, 3, 2, 4),    # discontinuous (rep = P)
+    ("laplace", 1, 1, 2, 6),    # m = 6: the lane-tile far kernel
     ("helmholtz", 1, 1, 2, 8),
     ("helmholtz", 3, 1, 2, 8),
     ("maxwell", 1, 1, 1, 6),
@@ -107,21 +108,15 @@ def _node_rel(got, ref):
     return float((np.abs(got - ref).max(axis=1) / np.maximum(mag, floor)).max())
 
 
-@pytest.mark.parametrize("variant", ["default", "stored", "tile"])
+@pytest.mark.parametrize("variant", ["fused", "stored"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "-".join(map(str, c)))
-def test_far_field_per_node(built, igb, case, variant, monkeypatch):
+def test_far_field_per_node(built, igb, case, variant):
     """The far-field kernel's own output: up (phase 3) and down after the far
     field and its transposed-slot sums (phase 4, h2.cpp:312-326) per cluster
     node against the oracle -- catches an error in the on-the-fly couplings
     (the Newton-refined rsqrt, the shifted dot-form distances) or in the slot
     bookkeeping that the aggregate matvec norm could hide."""
-    if variant == "tile":  # the lane-tile symmetric kernel (multi-GPU ranks, m = 6)
-        monkeypatch.setenv("IGB_FAR_KERNEL", "tile")
-        d = igb.Discretization(igb.make_sphere(), _pde(igb, case[0]), *case[1:4])
-        h = igb.H2Matrix(d, igb.H2Options(m=case[4], eta=1.6))
-        _, _, od, oh = built(*case)
-    else:
-        d, h, od, oh = built(*case, stored=variant == "stored")
+    d, h, od, oh = built(*case, stored=variant == "stored")
     rng = np.random.default_rng(7)
     x = rng.uniform(-1, 1, d.dof_count())
     if h.dtype == np.complex128:
