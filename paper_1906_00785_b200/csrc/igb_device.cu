@@ -1627,6 +1627,27 @@ __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict
   for (int i = 0; i < R; ++i) acc[i] = 0.0;
   const int q0 = LIST ? col_q0 : upper_start[t];
   const int ncol = ((LIST ? col_q1 : far_rs[t + 1]) - q0) * MM;
+  // the source node of column c (and its pair): read one chunk ahead, so the
+  // chunk's point loads depend on registers, not on loads of the same chunk
+  auto col_src = [&](int c, int& q, bool& sym) -> int {
+    const int qi = c / MM;
+    if constexpr (LIST) {
+      const int qe = __ldg(col_q + q0 + qi);
+      sym = qe >= 0;
+      q = qe >= 0 ? qe : ~qe;
+    } else {
+      sym = true;
+      q = q0 + qi;
+    }
+    return __ldg(far_b + q);
+  };
+  int s_nx[C], q_nx[C];
+  bool sym_nx[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const int c = 32 * k + lane;
+    s_nx[k] = c < ncol ? col_src(c, q_nx[k], sym_nx[k]) : t;
+  }
   // C columns per lane: each broadcast target row feeds C evaluations
   for (int c0 = 0; c0 < ncol; c0 += 32 * C) {
     double sx[C], sy[C], sz[C], xs[C], ns[C], ps[C];
@@ -1636,17 +1657,12 @@ __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict
     for (int k = 0; k < C; ++k) {
       const int c = c0 + 32 * k + lane;
       ok[k] = c < ncol;
-      const int qi = ok[k] ? c / MM : 0;
-      mu[k] = ok[k] ? c - qi * MM : 0;
-      if constexpr (LIST) {
-        const int qe = ok[k] ? __ldg(col_q + q0 + qi) : 0;
-        sym[k] = qe >= 0;
-        q[k] = qe >= 0 ? qe : ~qe;
-      } else {
-        sym[k] = true;
-        q[k] = q0 + qi;
-      }
-      const int s = ok[k] ? __ldg(far_b + q[k]) : t;
+      mu[k] = ok[k] ? c - (c / MM) * MM : 0;
+      q[k] = q_nx[k];
+      sym[k] = sym_nx[k];
+      const int s = s_nx[k];
+      const int cn = c + 32 * C;
+      s_nx[k] = cn < ncol ? col_src(cn, q_nx[k], sym_nx[k]) : t;
       const double* p = img + (static_cast<size_t>(s) * MM + mu[k]) * 3;
       sx[k] = __ldg(p) - cx;
       sy[k] = __ldg(p + 1) - cy;
