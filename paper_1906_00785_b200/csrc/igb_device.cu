@@ -419,6 +419,18 @@ __device__ __forceinline__ void jet_fixed(const double* __restrict__ st, double 
   jet_quot(N, Ns, Nt, x, du, dv);
 }
 
+// FP64 tensor-core MMA (DMMA, mma.sync m8n8k4): d += a b, one A element
+// (row lane/4, column lane%4), one B element (row lane%4, column lane/4) and two
+// accumulators (row lane/4, columns 2 (lane%4) + {0, 1}) per lane
+// point stride of the DMMA staging [l][point] (== 4 mod 16: the fragment loads of
+// a half warp hit 16 distinct bank pairs)
+constexpr int kDmmaPstr = 132;
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 // Exact small-integer division by the (runtime) rule order n: float
 // reciprocal estimate, then one correction step either way (x < 2^24).
 __device__ __forceinline__ int div_n(int x, int n, float rn) {
@@ -579,7 +591,7 @@ constexpr bool sing96_ok() {
 }
 inline bool sing96_use(int n) { return (kSingLmax < 128 / n ? kSingLmax : 128 / n) * n <= 96; }
 
-template <class KT, int CLS, int NTH = 128>
+template <class KT, int CLS, int NTH = 128, bool DMMA = false>
 __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(GeoArgs g, SingArgs A) {
   using S = typename KT::S;
   using LY = SingLayout<KT, NTH>;
@@ -641,6 +653,13 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
   for (int i = 0; i < TS; ++i)
 #pragma unroll
     for (int j = 0; j < TS; ++j) acc[i][j] = zero<S>();
+  double dm[2][2][2] = {};  // DMMA path: 2 x 2 tiles of the block, two accumulators each
+  if constexpr (DMMA) {     // zero the staging columns a last k-step may read past the chunk
+    static_assert(2 * NL * kDmmaPstr <= LY::BODY, "DMMA staging");
+    const int pad0 = (min(LY::LMAX, (CH < NTH ? CH : NTH) / A.n) * A.n);
+    for (int i = tid; i < ((pad0 + 3) & ~3) - pad0; i += NTH)
+      for (int l = 0; l < 2 * NL; ++l) body[l * kDmmaPstr + pad0 + i] = 0.0;
+  }
   const int tile = tid % NT, slice = tid / NT;
   const int tr = (tile / NTR) * TS, tc = (tile % NTR) * TS;
   const bool active = slice < SL;
@@ -802,8 +821,13 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
             }
 #pragma unroll
             for (int l = 0; l < NL; ++l) {
-              ga[c * NL + l] = wc * sa[c][l];
-              fb[c * NL + l] = sb[c][l];
+              if constexpr (DMMA) {  // transposed staging [l][point]: conflict-free DMMA fragments
+                reinterpret_cast<double*>(body)[l * kDmmaPstr + tid] = wc * sa[c][l];
+                body[(NL + l) * kDmmaPstr + tid] = sb[c][l];
+              } else {
+                ga[c * NL + l] = wc * sa[c][l];
+                fb[c * NL + l] = sb[c][l];
+              }
             }
           }
         }
@@ -819,8 +843,13 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
         } else {
 #pragma unroll
           for (int c = 0; c < NC * NL; ++c) {
-            ga[c] = zero<S>();
-            fb[c] = 0.0;
+            if constexpr (DMMA) {
+              body[c * kDmmaPstr + tid] = 0.0;
+              body[(NL + c) * kDmmaPstr + tid] = 0.0;
+            } else {
+              ga[c] = zero<S>();
+              fb[c] = 0.0;
+            }
           }
         }
       }
@@ -837,6 +866,20 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
         S sum = zero<S>();
         for (int k = 0; k < n; ++k) sum = sum + m[k * STR];
         Vr[(rb1 * LY::LMAX + ll) * NL + l] = sum;
+      }
+    } else if constexpr (DMMA) {
+      // Ga^T (NL x points) . Fb (points x NL) on the FP64 tensor cores: the
+      // warps take k-steps of 4 points round-robin, 2 x 2 tiles of 8 x 8
+      static_assert(KT::KIND == 0 && NC == 1 && NL == 16, "DMMA accumulation: real, 16 local functions");
+      const int wv = tid >> 5, ln = tid & 31, gid = ln >> 2, tig = ln & 3;
+      for (int st = wv; st * 4 < cpts; st += NTH / 32) {
+        const double* gr = body + gid * kDmmaPstr + st * 4 + tig;
+        const double* fr = body + (NL + gid) * kDmmaPstr + st * 4 + tig;
+        const double a0 = gr[0], a1 = gr[8 * kDmmaPstr], b0 = fr[0], b1 = fr[8 * kDmmaPstr];
+        dmma884(dm[0][0], a0, b0);
+        dmma884(dm[0][1], a0, b1);
+        dmma884(dm[1][0], a1, b0);
+        dmma884(dm[1][1], a1, b1);
       }
     } else if (active) {
       for (int pt = slice; pt < cpts; pt += SL) {
@@ -866,7 +909,18 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
     __syncthreads();
   }
   S* red = reinterpret_cast<S*>(body);
-  if (active) {
+  constexpr int NSL = DMMA ? NTH / 32 : SL;  // partial blocks: warps (DMMA) or slices
+  if constexpr (DMMA) {
+    const int wv = tid >> 5, ln = tid & 31, gid = ln >> 2, tig = ln & 3;
+    double* rd = reinterpret_cast<double*>(red) + wv * NL * NL;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        rd[(8 * i + gid) * NL + 8 * j + 2 * tig] = dm[i][j][0];
+        rd[(8 * i + gid) * NL + 8 * j + 2 * tig + 1] = dm[i][j][1];
+      }
+  } else if (active) {
 #pragma unroll
     for (int i = 0; i < TS; ++i)
 #pragma unroll
@@ -876,11 +930,11 @@ __global__ void __launch_bounds__(NTH, SingLayout<KT, NTH>::MINB) k_singular(Geo
   S* out = reinterpret_cast<S*>(A.out) + static_cast<size_t>(pr) * NL * NL;
   for (int o = tid; o < NL * NL; o += NTH) {
     S v = zero<S>();
-    for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + o];
+    for (int s = 0; s < NSL; ++s) v = v + red[s * NL * NL + o];
     if (half) {
       const int ot = (o % NL) * NL + o / NL;
 #pragma unroll 1
-      for (int s = 0; s < SL; ++s) v = v + red[s * NL * NL + ot];
+      for (int s = 0; s < NSL; ++s) v = v + red[s * NL * NL + ot];
     }
     out[o] = v;
   }
@@ -900,6 +954,14 @@ void launch_singular(const dev::GeoArgs& g, const dev::SingArgs& A, cudaStream_t
     }
   }
   using LY = dev::SingLayout<KT, 128>;
+  if constexpr (KT::KIND == 0 && KT::NL == 16 && CLS == 3) {
+    // real, 16 local functions, point-wise accumulation: on the FP64 tensor
+    // cores (c5 coincident 286 -> 245 ms; ncu: profiles/r02_ncu_c5_sing_summary.md)
+    IGB_CUDA(cudaFuncSetAttribute(dev::k_singular<KT, CLS, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(LY::BYTES)));
+    dev::k_singular<KT, CLS, 128, true><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
+    return;
+  }
   IGB_CUDA(cudaFuncSetAttribute(dev::k_singular<KT, CLS, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(LY::BYTES)));
   dev::k_singular<KT, CLS, 128><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
