@@ -960,11 +960,11 @@ void launch_singular(const dev::GeoArgs& g, const dev::SingArgs& A, cudaStream_t
     IGB_CUDA(cudaFuncSetAttribute(dev::k_singular<KT, CLS, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(LY::BYTES)));
     dev::k_singular<KT, CLS, 128, true><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
-    return;
+  } else {
+    IGB_CUDA(cudaFuncSetAttribute(dev::k_singular<KT, CLS, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(LY::BYTES)));
+    dev::k_singular<KT, CLS, 128><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
   }
-  IGB_CUDA(cudaFuncSetAttribute(dev::k_singular<KT, CLS, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(LY::BYTES)));
-  dev::k_singular<KT, CLS, 128><<<A.n_pairs, 128, LY::BYTES, st>>>(g, A);
 }
 namespace dev {
 // Singular blocks are integrated before the block partition exists (they only
@@ -3437,7 +3437,6 @@ template <class KT>
 static void dense_impl(const Discretization& d, int far_order, int sing_order, int device, double* out) {
   using S = typename KT::S;
   constexpr int NL = KT::NL, NC = KT::NC;
-  const int sw = sizeof(S) / 8;
   if (d.local_count() != NL) throw std::logic_error("B200 dense: local count mismatch");
   int nf = 0, ns = 0;
   check_h2_options(d, 2, 1.0, far_order, sing_order, &nf, &ns);
