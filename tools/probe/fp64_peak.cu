@@ -27,6 +27,28 @@ __global__ void dmma_kernel(double* out, int iters) {
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = c0[0] + c0[1] + c1[0] + c1[1] + c2[0] + c2[1] + c3[0] + c3[1];
 }
+// both pipes at once: each warp interleaves 4 DMMA chains with 8 DFMA chains
+__global__ void mixed_kernel(double* out, int iters, int dfma_per_mma) {
+  double a = threadIdx.x * 1e-3, bb = 1.0 - threadIdx.x * 1e-4;
+  double c0[2] = {0, 0}, c1[2] = {0, 0}, c2[2] = {0, 0}, c3[2] = {0, 0};
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double b = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(c0[0]), "+d"(c0[1]) : "d"(a), "d"(bb));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(c1[0]), "+d"(c1[1]) : "d"(a), "d"(bb));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(c2[0]), "+d"(c2[1]) : "d"(a), "d"(bb));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(c3[0]), "+d"(c3[1]) : "d"(a), "d"(bb));
+      for (int j = 0; j < dfma_per_mma; ++j) {
+        a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+        a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+      }
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = c0[0] + c0[1] + c1[0] + c1[1] + c2[0] + c2[1] + c3[0] + c3[1] +
+                                               a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
 int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   double* out; cudaMalloc(&out, sizeof(double) * nsm * 8 * 1024);
@@ -43,6 +65,16 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     double mflops = 2.0 * 256 * 4 * 8 * (double)(iters / 4) * blocks * (threads / 32);
     printf("DMMA m8n8k4: %.2f TFLOP/s (%.3f ms)\n", mflops / ms / 1e9, ms);
+  }
+  for (int dpm : {1, 2, 4, 8}) {  // DFMA groups (8 chains) per DMMA group (4 chains)
+    const int iters = 1000, blocks = nsm * 4, threads = 512;
+    mixed_kernel<<<blocks, threads>>>(out, 10, dpm);
+    cudaEventRecord(e0); mixed_kernel<<<blocks, threads>>>(out, iters, dpm); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double w = (double)iters * 8 * blocks;
+    const double mm = 2.0 * 256 * 4 * w * (threads / 32), ff = 2.0 * 8 * dpm * w * threads;
+    printf("mixed (%d DFMA x8 per 4 DMMA): DMMA %.2f + DFMA %.2f = %.2f TFLOP/s (%.3f ms)\n", dpm, mm / ms / 1e9,
+           ff / ms / 1e9, (mm + ff) / ms / 1e9, ms);
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
