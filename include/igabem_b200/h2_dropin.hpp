@@ -6,8 +6,10 @@
 // same members (rows, cols, apply, operator*, storage_report, nearfield_pairs,
 // farfield_pairs, tree), same exception types.  Assembly and matvec run on a
 // B200 through the C ABI in ../igabem_b200.h; the Discretization is flattened
-// through its public accessors (spaces.hpp:42-68, splines.hpp:53-67) and may be
-// destroyed afterwards (the reference keeps a raw pointer to it, h2.hpp:95).
+// through its public accessors (spaces.hpp:42-68, splines.hpp:53-67).  As with
+// the reference (h2.hpp:95), the Discretization must outlive the H2Matrix:
+// tree() returns an igabem::ClusterTree, which keeps a raw pointer to it
+// (h2.cpp:49, 89); the device operator itself no longer reads it.
 #pragma once
 
 #include <igabem/h2.hpp>
