@@ -287,6 +287,15 @@ def make_disc(igb, c):
     return igb.Discretization(igb.make_sphere(), pde, c["P"], c["rep"], c["L"])
 
 
+def load_pipes(name):
+    """ncu-measured FP64 / DMMA pipe utilisation of the kernels (committed capture)"""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"r02_ncu_pipes_{name}.json")) as f:
+            return json.load(f)["kernels"]
+    except Exception:
+        return {}
+
+
 def kernel_rooflines(h, c, disc, prof, iters, peaks, src, traffic):
     """Rooflines of the matvec graph's own kernels (timed serialised, CUDA
     events): algorithmic work per launch / average launch time."""
@@ -387,6 +396,10 @@ def run_b200(args, c, name):
                 "peak_source": "measured DFMA probe", "flops_per_launch": fl, "ms": ms, "points": sing_pts[cls],
                 "note": "per-point flop model of the unfactorised evaluation (bench.flops_per_point)",
                 "frac": fl / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, "traffic": None}
+    for k, v in load_pipes(name).items():  # hardware measure next to the model fractions
+        if k in rooflines:
+            rooflines[k]["ncu_fp64_pipe_pct"] = v["fp64_pipe_pct"]
+            rooflines[k]["ncu_dmma_pipe_pct"] = v["dmma_pipe_pct"]
     dom_key = dominant[len("matvec_"):] if dominant.startswith("matvec_") else dominant
     if dom_key not in rooflines:
         dom_key = "far_leaf_near" if "far_leaf_near" in rooflines else next(iter(rooflines))
