@@ -20,6 +20,17 @@
 namespace igb {
 namespace dev {
 
+// Block rows (near field, leaf blocks): the row of a test element holds its
+// blocks as columns j = k NL + lb (k-th block, trial function lb) for each test
+// function la.  Tiled layout: tiles of kRowTile columns, each tile stored
+// [la][column] contiguously -- a warp streams one tile per step and a tile is
+// one contiguous piece for a bulk copy.
+constexpr int kRowTile = 128;
+__host__ __device__ inline size_t row_tile_off(int len, int nl, int la, int j) {
+  const int t0 = (j / kRowTile) * kRowTile;
+  const int wt = len - t0 < kRowTile ? len - t0 : kRowTile;
+  return static_cast<size_t>(t0) * nl + static_cast<size_t>(la) * wt + (j - t0);
+}
 constexpr double kInv4Pi = 0.079577471545947667884;  // 1 / (4 pi)
 constexpr int kCellStride = 104;                       // 100 coefficients + u0, v0 (+pad)
 

@@ -175,6 +175,16 @@ T* H2Device::upload(const std::vector<T>& v) {
   return p;
 }
 
+// default fraction of each leaf target's upper far pairs applied as stored
+// element blocks (IGB_H2_LEAF_BLOCKS overrides): warp-specialised leaf kernel
+// (c5: leaf kernel 7.38 ms without blocks, 6.14 / 5.84 / 5.81 ms at 0.4 / 0.5 /
+// 0.6) and the one-warp-per-target fused kernel (c5: 7.30 -> 6.71 ms at 0.4)
+constexpr double kLeafBlockFractionWs = 0.5, kLeafBlockFraction = 0.4;
+// IGB_H2_LEAF_WS=0: the one-warp-per-target fused leaf kernel instead of k_leaf_ws
+static bool leaf_ws_enabled() {
+  const char* e = getenv("IGB_H2_LEAF_WS");
+  return e == nullptr || atoi(e) != 0;
+}
 static unsigned grid_for(long long n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
 H2Device::H2Device(std::shared_ptr<const Discretization> d, int m, double eta, int far_order, int sing_order,
@@ -515,6 +525,60 @@ void H2Device::stage_plan() {
           if (!has[e]) rest.push_back(e);
         n_near_rest_ = static_cast<int>(rest.size());
         d_near_rest_ = upload(rest);
+        // Leaf blocks: the fused leaf kernel is FP64-bound and leaves HBM idle, so
+        // a fraction of every leaf target's upper pairs (the last ones of its
+        // row) is applied as stored element blocks M_t K M_s^T instead of being
+        // evaluated (k_leaf_blocks; streamed once per unordered pair for both
+        // directions).  IGB_H2_LEAF_BLOCKS: the fraction (0 disables).
+        double frac = (NL == 16 && leaf_ws_enabled()) ? kLeafBlockFractionWs : kLeafBlockFraction;
+        if (const char* env = getenv("IGB_H2_LEAF_BLOCKS")) frac = atof(env);
+        frac = std::min(1.0, std::max(0.0, frac));
+        const int ne = d.element_count(), leaf_off = P.level_offset[P.depth];
+        auto leaf_of = [&](int e) { return (e / epp) * P.npp + leaf_off + e % epp; };
+        std::vector<int> lb_rs(ne + 1, 0), upper_end(P.far_row_start.begin() + 1, P.far_row_start.end());
+        for (; frac > 0.0; frac *= 0.5) {  // within a quarter of the free device memory
+          for (int e = 0; e < ne; ++e) {
+            const int t = leaf_of(e), nup = P.far_row_start[t + 1] - P.far_upper_start[t];
+            lb_rs[e + 1] = lb_rs[e] + std::min(nup, static_cast<int>(frac * nup + 0.5));
+          }
+          size_t free_b = 0, total_b = 0;
+          IGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+          const size_t fixed = (static_cast<size_t>(Lp.near_row.size()) * NL * NL + P.far_a.size() * mm) * 8;
+          if (static_cast<double>(lb_rs[ne]) * NL * NL * 8 <= 0.25 * (static_cast<double>(free_b) - fixed)) break;
+        }
+        if (frac > 0.0 && lb_rs[ne] > 0) {
+          const int nb = lb_rs[ne];
+          std::vector<int> nt(nb), ns(nb), eb(nb), in_rs(ne + 1, 0), in_k(nb);
+#pragma omp parallel for schedule(static)
+          for (int e = 0; e < ne; ++e) {
+            const int t = leaf_of(e), cnt = lb_rs[e + 1] - lb_rs[e];
+            upper_end[t] -= cnt;
+            for (int k = 0; k < cnt; ++k) {
+              const int sq = P.far_b[upper_end[t] + k];
+              nt[lb_rs[e] + k] = t;
+              ns[lb_rs[e] + k] = sq;
+              eb[lb_rs[e] + k] = (sq / P.npp) * epp + (sq % P.npp - leaf_off);
+            }
+          }
+          for (int k = 0; k < nb; ++k) ++in_rs[eb[k] + 1];
+          for (int e = 0; e < ne; ++e) in_rs[e + 1] += in_rs[e];
+          {
+            std::vector<int> fill(in_rs.begin(), in_rs.end() - 1);
+            for (int k = 0; k < nb; ++k) in_k[fill[eb[k]]++] = k;  // ascending k: fixed summation order
+          }
+          n_leaf_blocks_ = nb;
+          leaf_block_bytes_ = static_cast<size_t>(nb) * NL * NL * 8;
+          sym_pairs_[0] -= nb;
+          d_upper_end_ = upload(upper_end);
+          d_lb_rs_ = upload(lb_rs);
+          d_lb_eb_ = upload(eb);
+          d_lb_nt_ = upload(nt);
+          d_lb_ns_ = upload(ns);
+          d_lb_in_rs_ = upload(in_rs);
+          d_lb_in_k_ = upload(in_k);
+          d_lb_blk_ = dalloc<double>(static_cast<size_t>(nb) * NL * NL);
+          d_lb_tslot_ = dalloc<double>(static_cast<size_t>(nb) * NL);
+        }
       }
       if (Lp.world > 1 && sym_far_ && m <= 5) {  // per-target column lists for k_far_col_list
         std::vector<int> col_rs(1, 0), col_q;
@@ -637,6 +701,21 @@ void H2Device::launch_plan_phase(cudaEvent_t* ev, int& launched) {
                                                        as_.node_sx, as_.node_sy, pd, d_cells_, d_img_);
     ++launched;
     IGB_CUDA(cudaGetLastError());
+  }
+  if (n_leaf_blocks_ > 0) {
+    if constexpr (KT::KIND == 0 && NL <= 16) {
+      const int nb = static_cast<int>(n_leaf_blocks_);
+      auto go = [&](auto kern, int M_) {
+        const size_t smem = 4 * static_cast<size_t>(2 * NL * M_ * M_ + M_ * M_ * M_ * M_ + M_ * M_ * NL + 6 * M_ * M_) * 8;
+        IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<grid_for(nb, 4), 128, smem, stream_>>>(nb, d_lb_nt_, d_lb_ns_, d_lb_rs_, d.elements_per_patch(), P.npp,
+                                                      P.level_offset[P.depth], d_img_, d_mom_, d_lb_blk_);
+      };
+      if (m == 4) go(k_leaf_blocks<4, NL>, 4);
+      else go(k_leaf_blocks<5, NL>, 5);
+      ++launched;
+      IGB_CUDA(cudaGetLastError());
+    }
   }
   IGB_CUDA(cudaEventRecord(ev[kEvImages], stream_));
   if (nfarp > 0 && stored_couplings()) {  // fused mode evaluates the couplings inside the matvec
@@ -853,10 +932,10 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
       const double* upd = reinterpret_cast<const double*>(up);
       if (far_col_) {  // one GPU, m <= 5 (graphs without the level split: depth 0)
         switch (m) {
-          case 2: k_far_col<2, 4, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-          case 3: k_far_col<3, 4, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-          case 4: k_far_col<4, 3, 2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
-          default: k_far_col<5, 2, 2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+          case 2: k_far_col<2, 4, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_ + 1, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+          case 3: k_far_col<3, 4, 1><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_ + 1, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+          case 4: k_far_col<4, 3, 2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_ + 1, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
+          default: k_far_col<5, 2, 2><<<gsym, 256, 0, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_ + 1, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_); break;
         }
       } else if (m <= 5) {  // ranks: column stream over the rank's pair lists
 #define IGB_FCL(M_, MB_, C_)                                                                                 \
@@ -949,7 +1028,8 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
   }
   if (pev == nullptr) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));  // near rows (side stream) done
   pdl_launch(k_leaf_down<S, NL>, grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s, 
-      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
+      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc,
+      static_cast<const int*>(nullptr), static_cast<const int*>(nullptr), static_cast<const S*>(nullptr));
   ++launches;
   mark(7);
   pdl_launch(k_scatter<S>, grid_for(d.dof_count(), 256), 256, 0, s, d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
@@ -995,6 +1075,8 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   (void)nloc;
   (void)coef;
   const bool fused = KT::KIND == 0 && NL <= 16 && n_near_rest_ >= 0;
+  // warp-specialised leaf kernel (k_leaf_ws): far warps + stream warps per SM
+  const bool leaf_ws = fused && leaf_ws_enabled() && NL == 16 && (m == 4 || m == 5);
   // profiling (prof != nullptr): the same kernels serialised on s, an event
   // after each one, so every graph kernel is timed on its own
   cudaStream_t side1 = prof ? s : side_, side2 = prof ? s : side2_;
@@ -1019,18 +1101,22 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   if (!prof) IGB_CUDA(cudaEventRecord(ev_join_, side_));
   const long long ndown = static_cast<long long>(P.n_nodes) * rows;
   pdl_launch(k_leaf_up_x<S, NL>, grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s, 
-      nel, rows, epp, npp, P.level_offset[L], d_mom_, x, d_l2g_, d_lsign_, up, down, ndown);
+      nel, rows, epp, npp, P.level_offset[L], d_mom_, x, d_l2g_, d_lsign_, up, down, ndown,
+      static_cast<S*>(leaf_ws ? coef : nullptr));
   ++launches;
   tick("leaf_up");
   if (!prof) {
     IGB_CUDA(cudaEventRecord(ev_fork2_, s));
     IGB_CUDA(cudaStreamWaitEvent(side2_, ev_fork2_, 0));
   }
+  // leaf blocks: off for the far-field introspection (phase 4 output of all pairs)
+  const bool blocks = fused && n_leaf_blocks_ > 0 && !far_only_;
+  const int* far_end = d_far_rs_ + 1;
   auto far_sym = [&](cudaStream_t st, int n, const int* targets) {
     if (n == 0) return;
     const unsigned g = grid_for(static_cast<long long>(n) * 32, 256);
     if (far_col_) {  // column stream: m <= 5
-#define IGB_FC(M_, MB_, C_) k_far_col<M_, MB_, C_><<<g, 256, 0, st>>>(n, targets, d_upper_start_, d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_)
+#define IGB_FC(M_, MB_, C_) k_far_col<M_, MB_, C_><<<g, 256, 0, st>>>(n, targets, d_upper_start_, far_end, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_)
       switch (m) {
         case 2: IGB_FC(2, 4, 1); break;
         case 3: IGB_FC(3, 4, 1); break;
@@ -1074,14 +1160,32 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   if (fused) {
     if constexpr (KT::KIND == 0 && NL <= 16) {
       const long long nw = static_cast<long long>(n_sym_fine_) + n_near_rest_;
+      LeafBlocks lbk{far_end, nullptr, nullptr, nullptr, nullptr};
+      if (blocks) lbk = LeafBlocks{d_upper_end_, d_lb_rs_, d_lb_eb_, d_lb_blk_, d_lb_tslot_};
       auto fused_launch = [&](auto kern) {
         kern<<<grid_for(nw * 32, 256), 256, 0, s>>>(
             n_sym_fine_, d_sym_fine_, n_near_rest_, d_near_rest_, epp, npp, P.level_offset[L], d_upper_start_,
-            d_far_rs_, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, d_near_rs_, d_near_b_,
+            lbk, d_far_b_, d_trans_, d_img_, upd, dn, d_slot_, d_owned_, d_near_rs_, d_near_b_,
             reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
             reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
       };
-      if (m == 4)
+      if constexpr (NL == 16) {
+        if (leaf_ws) {
+          auto ws_launch = [&](auto kern, size_t smem) {
+            int nsm = 0;
+            IGB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_));
+            IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            kern<<<nsm, 32 * (ws::kFarWarps + ws::kStreamWarps), smem, s>>>(
+                n_sym_fine_, d_sym_fine_, d.element_count(), d_upper_start_, lbk, d_far_b_, d_trans_, d_img_, upd, dn,
+                d_slot_, d_near_rs_, d_near_b_, reinterpret_cast<const double*>(d_near_),
+                reinterpret_cast<const double*>(coef), reinterpret_cast<double*>(nrows));
+          };
+          if (m == 4) ws_launch(k_leaf_ws<4, NL, 2>, ws::Layout<4, NL>::BYTES);
+          else ws_launch(k_leaf_ws<5, NL, 2>, ws::Layout<5, NL>::BYTES);
+        }
+      }
+      if (leaf_ws) {
+      } else if (m == 4)
         fused_launch(k_far_col_near<4, NL, 3, 2>);
       else
         fused_launch(k_far_col_near<5, NL, 2, 2>);
@@ -1108,7 +1212,9 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   tick("downward_leaf");
   if (!prof) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
   pdl_launch(k_leaf_down<S, NL>, grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s, 
-      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc);
+      nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc,
+      static_cast<const int*>(blocks ? d_lb_in_rs_ : nullptr), static_cast<const int*>(blocks ? d_lb_in_k_ : nullptr),
+      blocks ? reinterpret_cast<const S*>(d_lb_tslot_) : static_cast<const S*>(nullptr));
   tick("leaf_down");
   pdl_launch(k_scatter<S>, grid_for(d.dof_count(), 256), 256, 0, s, d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
   launches += 2;
@@ -1276,6 +1382,8 @@ void H2Device::far_field(const double* x, double* up_out, double* down_out) {
   }
   far_only_ = false;
   IGB_CUDA(cudaStreamSynchronize(stream_));
+  if (n_leaf_blocks_ > 0)  // the blocked pairs' slots were written here; apply() never rewrites them
+    IGB_CUDA(cudaMemsetAsync(d_slot_, 0, plan_.far_a.size() * static_cast<size_t>(plan_.m) * plan_.m * sizeof(double), stream_));
   const size_t n = static_cast<size_t>(plan_.n_nodes) * nch_ * plan_.m * plan_.m * sw;
   if (up_out) IGB_CUDA(cudaMemcpy(up_out, d_up_, n, cudaMemcpyDeviceToHost));
   if (down_out) IGB_CUDA(cudaMemcpy(down_out, d_down_, n, cudaMemcpyDeviceToHost));
@@ -1391,7 +1499,7 @@ void H2Device::near_blocks(long long first, long long count, double* out) const 
     const int e = plan_.near_a[q], rs = plan_.near_row_start[e], cnt = plan_.near_row_start[e + 1] - rs;
     for (int la = 0; la < nl; ++la)
       for (int lb = 0; lb < nl; ++lb) {
-        const size_t src = static_cast<size_t>(rs - r0) * nl * nl + (static_cast<size_t>(la) * cnt + (q - rs)) * nl + lb;
+        const size_t src = static_cast<size_t>(rs - r0) * nl * nl + row_tile_off(cnt * nl, nl, la, static_cast<int>(q - rs) * nl + lb);
         const size_t dst = (static_cast<size_t>(q - first) * nl + la) * nl + lb;
         for (int c = 0; c < sw; ++c) out[dst * sw + c] = buf[src * sw + c];
       }

@@ -78,6 +78,9 @@ class H2Device {
   void far_field(const double* x, double* up_out, double* down_out);
   // unordered far pairs the symmetric far kernels evaluate: [leaf level, above]
   long long sym_pairs(int which) const { return sym_pairs_[which]; }
+  // leaf-level far pairs applied as stored element blocks (LeafBlocks) and their bytes
+  long long leaf_block_pairs() const { return n_leaf_blocks_; }
+  size_t leaf_block_bytes() const { return leaf_block_bytes_; }
   // `steps` x (device assembly + `matvecs` matvecs), CUDA events; returns ms
   double bench_steps(int steps, int matvecs, double* assembly_ms);
   int assembly_kernel_launches() const { return assembly_kernels_; }
@@ -161,6 +164,14 @@ class H2Device {
   int n_near_rest_ = -1;  // fused leaf far field + near rows: elements without leaf targets (-1: off)
   int* d_near_rest_ = nullptr;
   double* d_slot_ = nullptr;
+  // leaf blocks (fused leaf kernel): blocked unordered leaf pairs in CSR by the
+  // lower element, their nodes (assembly), the incoming lists of the upper
+  // elements, blocks in the block-row layout, transposed products
+  long long n_leaf_blocks_ = 0;
+  size_t leaf_block_bytes_ = 0;
+  int *d_upper_end_ = nullptr, *d_lb_rs_ = nullptr, *d_lb_eb_ = nullptr, *d_lb_nt_ = nullptr, *d_lb_ns_ = nullptr;
+  int *d_lb_in_rs_ = nullptr, *d_lb_in_k_ = nullptr;
+  double *d_lb_blk_ = nullptr, *d_lb_tslot_ = nullptr;
   int *d_far_a_ = nullptr;
   int *d_dof_start_ = nullptr, *d_dof_inc_ = nullptr;
   int *d_near_ea_ = nullptr, *d_el_ = nullptr, *d_pack_nodes_ = nullptr, *d_unpack_nodes_ = nullptr;
@@ -168,7 +179,7 @@ class H2Device {
   double *d_loc_sign_ = nullptr, *d_send_ = nullptr, *d_recv_ = nullptr;
   double *d_tl_ = nullptr, *d_tr_ = nullptr;
   // operator data
-  double* d_near_ = nullptr;   // row layout [e][la][k][lb], Scalar
+  double* d_near_ = nullptr;   // block rows per test element (tiled layout, row_tile_off), Scalar
   double* d_far_ = nullptr;    // [q][mu][nu], Scalar
   double* d_mom_ = nullptr;    // [e][l][row], real
   double* d_img_ = nullptr;    // [node][nu][3]

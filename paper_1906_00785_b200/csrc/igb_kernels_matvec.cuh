@@ -43,12 +43,14 @@ __global__ void k_leaf_up(int n_el, const int* __restrict__ el, int rows, int ep
 template <class S, int NL>
 __global__ void k_leaf_up_x(int n_el, int rows, int epp, int npp, int leaf_off, const double* __restrict__ mom,
                             const S* __restrict__ x, const int* __restrict__ l2g, const double* __restrict__ sg,
-                            S* __restrict__ up, S* __restrict__ down, long long ndown) {
+                            S* __restrict__ up, S* __restrict__ down, long long ndown,
+                            S* __restrict__ coef_out) {
   pdl_entry();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx < ndown) down[idx] = zero<S>();
   if (idx >= static_cast<long long>(n_el) * rows) return;
   const int e = static_cast<int>(idx / rows), r = static_cast<int>(idx % rows);
+  if (coef_out != nullptr && r < NL) coef_out[e * NL + r] = x[l2g[e * NL + r]] * sg[e * NL + r];  // rows >= NL
   S acc = zero<S>();
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
@@ -680,9 +682,11 @@ __device__ __forceinline__ void col_reduce_rows(double (&acc)[ColRows<MM>::R], i
 // (col_q[col_rs[w] ..]): q >= 0 a pair with an owned source s > t (symmetric:
 // the transposed product goes to the slot of (s, t)), ~q a pair whose source
 // is another rank's node (one-sided: no slot; that rank evaluates its own side)
+// far_end[t]: end of the target's evaluated upper pairs -- its row end
+// (far_rs + 1) or, for leaf targets with blocked pairs (LeafBlocks), before them
 template <int M, int C, bool LIST = false>
 __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict__ sh,
-                                             const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+                                             const int* __restrict__ upper_start, const int* __restrict__ far_end,
                                              const int* __restrict__ far_b, const int* __restrict__ trans,
                                              const double* __restrict__ img, const double* __restrict__ up,
                                              double* __restrict__ down, double* __restrict__ slot,
@@ -707,7 +711,7 @@ __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict
 #pragma unroll
   for (int i = 0; i < R; ++i) acc[i] = 0.0;
   const int q0 = LIST ? col_q0 : upper_start[t];
-  const int ncol = ((LIST ? col_q1 : far_rs[t + 1]) - q0) * MM;
+  const int ncol = ((LIST ? col_q1 : far_end[t]) - q0) * MM;
   // the source node of column c (and its pair): read one chunk ahead, so the
   // chunk's point loads depend on registers, not on loads of the same chunk
   auto col_src = [&](int c, int& q, bool& sym) -> int {
@@ -781,14 +785,14 @@ __device__ __forceinline__ void far_col_body(int t, int lane, double* __restrict
 template <int M, int MINB, int C>
 __global__ void __launch_bounds__(256, MINB) k_far_col(int n_targets, const int* __restrict__ targets,
                                                       const int* __restrict__ upper_start,
-                                                      const int* __restrict__ far_rs, const int* __restrict__ far_b,
+                                                      const int* __restrict__ far_end, const int* __restrict__ far_b,
                                                       const int* __restrict__ trans, const double* __restrict__ img,
                                                       const double* __restrict__ up, double* __restrict__ down,
                                                       double* __restrict__ slot) {
   __shared__ __align__(16) double sh[8][(5 * M * M + 1) / 2 * 2];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= n_targets) return;
-  far_col_body<M, C>(targets[warp], threadIdx.x & 31, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img,
+  far_col_body<M, C>(targets[warp], threadIdx.x & 31, sh[threadIdx.x >> 5], upper_start, far_end, far_b, trans, img,
                      up, down, slot);
 }
 
@@ -882,43 +886,85 @@ __global__ void k_unpack(int n, const int* __restrict__ nodes, int rows, const S
 }
 
 // near-field rows per test element (h2.cpp:349-357); one warp per element,
-// streaming its contiguous row [la][k][lb]
+// streaming its contiguous row (tiled block-row layout, row_tile_off)
 // FROM_X: coefficients gathered inline from x (l2g, signs) instead of coef
-template <class S, int NL, bool FROM_X>
-__device__ __forceinline__ void near_row(int e, int lane, const int* __restrict__ near_rs,
-                                         const int* __restrict__ near_b, const S* __restrict__ blk,
-                                         const S* __restrict__ coef, S* __restrict__ rows_out,
-                                         const int* __restrict__ l2g, const double* __restrict__ sg) {
+// SYM (leaf blocks, below): the row's blocks are those of unordered pairs
+// (e, f), f > e; lane j = column (k, lb) also forms the transposed product
+// sum_la blk[la][j] c_e[la] -- a lane-local sum -- into tslot[row start NL + j],
+// which the leaf transform of element f adds.  xt: c_e in shared memory.
+template <class S, int NL, bool FROM_X, bool SYM = false>
+__device__ __forceinline__ void near_row_seg(S (&acc)[NL], int e, int lane, const int* __restrict__ near_rs,
+                                             const int* __restrict__ near_b, const S* __restrict__ blk,
+                                             const S* __restrict__ coef, const int* __restrict__ l2g,
+                                             const double* __restrict__ sg, S* __restrict__ tslot = nullptr,
+                                             S* __restrict__ xt = nullptr) {
   auto cf = [&](int k) -> S {
     if constexpr (FROM_X) return coef[l2g[k]] * sg[k];
     else return coef[k];
   };
   const int rs = near_rs[e], cnt = near_rs[e + 1] - rs;
+  if (SYM && cnt == 0) return;
   const int len = cnt * NL;
   const S* base = blk + static_cast<size_t>(rs) * NL * NL;
-  S acc[NL];
-#pragma unroll
-  for (int l = 0; l < NL; ++l) acc[l] = zero<S>();
+  if constexpr (SYM) {
+    __syncwarp();
+    if (lane < NL) xt[lane] = cf(e * NL + lane);
+    __syncwarp();
+  }
   constexpr int U = (NL <= 9) ? 4 : 2;
+  static_assert(kRowTile % 32 == 0, "a lane's columns of one step lie in whole tiles");
   int j = lane;
   for (; j + 32 * (U - 1) < len; j += 32 * U) {
-    S xv[U];
+    S xv[U], ps[U];
+    const S* tb[U];  // column j + 32 u of its tile (row_tile_off): tile base + la * tile width
+    int wt[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int jj = j + 32 * u, k = jj / NL, lb = jj - k * NL;
       xv[u] = cf(near_b[rs + k] * NL + lb);
+      ps[u] = zero<S>();
+      const int t0 = jj & ~(kRowTile - 1);
+      wt[u] = min(kRowTile, len - t0);
+      tb[u] = base + static_cast<size_t>(t0) * NL + (jj - t0);
     }
 #pragma unroll
-    for (int la = 0; la < NL; ++la)
+    for (int la = 0; la < NL; ++la) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) fmac(acc[la], ldg_s(base + static_cast<size_t>(la) * len + j + 32 * u), xv[u]);
+      for (int u = 0; u < U; ++u) {
+        const S v = ldg_s(tb[u] + la * wt[u]);
+        fmac(acc[la], v, xv[u]);
+        if constexpr (SYM) fmac(ps[u], v, xt[la]);
+      }
+    }
+    if constexpr (SYM) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) tslot[static_cast<size_t>(rs) * NL + j + 32 * u] = ps[u];
+    }
   }
   for (; j < len; j += 32) {
     const int k = j / NL, lb = j - k * NL;
     const S xv = cf(near_b[rs + k] * NL + lb);
+    S ps = zero<S>();
+    const int t0 = j & ~(kRowTile - 1), wt = min(kRowTile, len - t0);
+    const S* tb = base + static_cast<size_t>(t0) * NL + (j - t0);
 #pragma unroll
-    for (int la = 0; la < NL; ++la) fmac(acc[la], ldg_s(base + static_cast<size_t>(la) * len + j), xv);
+    for (int la = 0; la < NL; ++la) {
+      const S v = ldg_s(tb + la * wt);
+      fmac(acc[la], v, xv);
+      if constexpr (SYM) fmac(ps, v, xt[la]);
+    }
+    if constexpr (SYM) tslot[static_cast<size_t>(rs) * NL + j] = ps;
   }
+}
+template <class S, int NL, bool FROM_X>
+__device__ __forceinline__ void near_row(int e, int lane, const int* __restrict__ near_rs,
+                                         const int* __restrict__ near_b, const S* __restrict__ blk,
+                                         const S* __restrict__ coef, S* __restrict__ rows_out,
+                                         const int* __restrict__ l2g, const double* __restrict__ sg) {
+  S acc[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) acc[l] = zero<S>();
+  near_row_seg<S, NL, FROM_X>(acc, e, lane, near_rs, near_b, blk, coef, l2g, sg);
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
     const S a = warp_sum(acc[l]);
@@ -939,29 +985,286 @@ __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict
 // Leaf-level column-stream far field fused with the near rows (single GPU): as
 // the HBM-bound rows run at the tail of each warp while other warps of the SM
 // are still in the FP64-bound far loop.
+// LeafBlocks: the last upper pairs of every leaf target are not evaluated but
+// stored as element blocks M_t K M_s^T (k_leaf_blocks) and streamed like near
+// blocks, each once for both directions (near_row_seg SYM) -- the FP64-bound
+// kernel leaves HBM idle, so part of its work moves there.
+struct LeafBlocks {
+  const int* far_end;   // per node: end of the evaluated upper pairs
+  const int* rs;        // per element: first blocked pair (CSR), null: none
+  const int* eb;        // source element of each blocked pair
+  const double* blk;    // element rows, tiled block-row layout
+  double* tslot;        // transposed products [pair][lb]
+};
 template <int M, int NL, int MINB, int C>
 __global__ void __launch_bounds__(256, MINB) k_far_col_near(
     int n_fine, const int* __restrict__ fine, int n_rest, const int* __restrict__ rest, int epp, int npp,
-    int leaf_off, const int* __restrict__ upper_start, const int* __restrict__ far_rs,
+    int leaf_off, const int* __restrict__ upper_start, LeafBlocks lb,
     const int* __restrict__ far_b, const int* __restrict__ trans, const double* __restrict__ img,
     const double* __restrict__ up, double* __restrict__ down, double* __restrict__ slot,
     const unsigned char* __restrict__ /*owned: single GPU*/, const int* __restrict__ near_rs,
     const int* __restrict__ near_b, const double* __restrict__ blk, const double* __restrict__ x,
     double* __restrict__ rows_out, const int* __restrict__ l2g, const double* __restrict__ sg) {
   __shared__ __align__(16) double sh[8][(5 * M * M + 1) / 2 * 2];
+  static_assert(5 * M * M >= NL, "shared slab holds the element's coefficients");
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   int e;
   if (warp < n_fine) {
     const int t = fine[warp];
-    far_col_body<M, C>(t, lane, sh[threadIdx.x >> 5], upper_start, far_rs, far_b, trans, img, up, down, slot);
+    far_col_body<M, C>(t, lane, sh[threadIdx.x >> 5], upper_start, lb.far_end, far_b, trans, img, up, down, slot);
     e = (t / npp) * epp + (t % npp - leaf_off);
   } else if (warp < n_fine + n_rest) {
     e = rest[warp - n_fine];
   } else {
     return;
   }
-  near_row<double, NL, true>(e, lane, near_rs, near_b, blk, x, rows_out, l2g, sg);
+  double acc[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+  near_row_seg<double, NL, true>(acc, e, lane, near_rs, near_b, blk, x, l2g, sg);
+  if (lb.rs != nullptr)
+    near_row_seg<double, NL, true, true>(acc, e, lane, lb.rs, lb.eb, lb.blk, x, l2g, sg, lb.tslot,
+                                         sh[threadIdx.x >> 5]);
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const double a = warp_sum(acc[l]);
+    if (lane == 0) rows_out[static_cast<size_t>(e) * NL + l] = a;
+  }
+}
+
+// ---- warp-specialised leaf kernel (single GPU, NL = 16) ------------------
+// One persistent 512-thread CTA per SM: twelve far warps run the column-stream
+// far field over the leaf targets while four stream warps move the near rows
+// and the leaf blocks through a shared-memory ring with bulk asynchronous copies
+// (cp.async.bulk + mbarrier, no registers in flight), so the FP64 pipe and HBM
+// are busy at the same time on every SM -- inside one warp the two phases only
+// alternate.  A slice = one tile of a block row (row_tile_off: kRowTile columns
+// x NL test functions, contiguous: one copy) plus the coefficient vectors of
+// its blocks' source elements (one copy each).
+namespace ws {
+// 12 + 4 warps, 3 stages of one 17 KB tile each per stream warp (c5: leaf kernel
+// 5.84 ms; 13 + 3 warps 6.41, 14 + 2 warps 8.33)
+constexpr int kStreamWarps = 4, kFarWarps = 16 - kStreamWarps, kStages = 3;
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  const unsigned a = smem_u32(bar);
+  while (!ok)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+}
+// streamed once: evict-first in L2 (the far warps' node images and moments stay)
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// 16 B per lane, completion counted by the stage's mbarrier
+__device__ __forceinline__ void cp16_g2s(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+template <int M, int NL>
+struct Layout {
+  static constexpr int SLAB = (5 * M * M + 1) / 2 * 2;             // far warp: target rows + moments
+  static constexpr int STAGE = (NL + 1) * kRowTile;                // stream stage: tile [NL][w] + coefficients [w]
+  static constexpr int FAR0 = 0;
+  static constexpr int RING0 = (kFarWarps * SLAB + 15) / 16 * 16;  // doubles, 128 B aligned
+  static constexpr int XT0 = RING0 + kStreamWarps * kStages * STAGE;
+  static constexpr int DESC0 = XT0 + kStreamWarps * NL;            // int4 per stage
+  static constexpr int BAR0 = DESC0 + kStreamWarps * kStages * 2;
+  static constexpr int TOTAL = BAR0 + kStreamWarps * kStages;
+  static constexpr size_t BYTES = static_cast<size_t>(TOTAL) * 8;
+};
+}  // namespace ws
+
+template <int M, int NL, int C>
+__global__ void __launch_bounds__(32 * (ws::kFarWarps + ws::kStreamWarps), 1) k_leaf_ws(
+    int n_fine, const int* __restrict__ fine, int ne, const int* __restrict__ upper_start, LeafBlocks lb,
+    const int* __restrict__ far_b, const int* __restrict__ trans, const double* __restrict__ img,
+    const double* __restrict__ up, double* __restrict__ down, double* __restrict__ slot,
+    const int* __restrict__ near_rs, const int* __restrict__ near_b, const double* __restrict__ blk,
+    const double* __restrict__ coef, double* __restrict__ rows_out) {
+  using LY = ws::Layout<M, NL>;
+  constexpr int W = kRowTile, NS = ws::kStages;
+  static_assert(NL % 2 == 0 && W % NL == 0 && W % 64 == 0, "16 B coefficient pairs inside one block");
+  extern __shared__ __align__(128) double wsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < ws::kFarWarps) {  // ---- far warps
+    double* sh = wsm + LY::FAR0 + warp * LY::SLAB;
+    for (int i = blockIdx.x * ws::kFarWarps + warp; i < n_fine; i += gridDim.x * ws::kFarWarps) {
+      far_col_body<M, C>(fine[i], lane, sh, upper_start, lb.far_end, far_b, trans, img, up, down, slot);
+      __syncwarp();  // the slab is rewritten for the next target
+    }
+    return;
+  }
+  // ---- stream warps
+  const int sw = warp - ws::kFarWarps;
+  double* ring = wsm + LY::RING0 + sw * NS * LY::STAGE;
+  double* xt = wsm + LY::XT0 + sw * NL;
+  int4* desc = reinterpret_cast<int4*>(wsm + LY::DESC0) + sw * NS;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + LY::BAR0) + sw * NS;
+  if (lane == 0) {
+    for (int i = 0; i < NS; ++i) ws::mbar_init(bar + i, 33);  // expect_tx arrive + one per lane (coefficients)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  // slice generator (warp-uniform): elements e = first, first + stride, ...;
+  // segment 0 the near row, segment 1 the leaf blocks of e.  The row extents of
+  // the next element are read one element ahead.
+  const int stride = gridDim.x * ws::kStreamWarps;
+  int g_e = blockIdx.x * ws::kStreamWarps + sw, g_seg = 0, g_j0 = 0, g_rs = 0, g_len = 0, g_len1 = 0, g_rs1 = 0;
+  int n_rs = 0, n_re = 0, n_rs1 = 0, n_re1 = 0;
+  auto fetch_item = [&](int e) {
+    if (e < ne) {
+      n_rs = near_rs[e];
+      n_re = near_rs[e + 1];
+      n_rs1 = lb.rs ? lb.rs[e] : 0;
+      n_re1 = lb.rs ? lb.rs[e + 1] : 0;
+    }
+  };
+  auto load_item = [&]() {  // element g_e from the prefetched extents; prefetch the next
+    g_rs = n_rs;
+    g_len = (n_re - n_rs) * NL;
+    g_rs1 = n_rs1;
+    g_len1 = (n_re1 - n_rs1) * NL;
+    g_seg = 0;
+    g_j0 = 0;
+    fetch_item(g_e + stride);
+  };
+  fetch_item(g_e);
+  if (g_e < ne) load_item();
+  const unsigned long long pol = ws::policy_evict_first();
+  // source elements of the blocks holding this lane's coefficient pairs (columns
+  // 2 lane + 64 h + {0, 1}) of the current slice, read one slice ahead
+  constexpr int H = W / 64;
+  int pf_e[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) pf_e[h] = 0;
+  auto prefetch_src = [&]() {
+    if (g_e >= ne) return;
+    const int rs = g_seg ? g_rs1 : g_rs, len = g_seg ? g_len1 : g_len;
+    const int w = min(W, len - g_j0);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int c = 2 * lane + 64 * h;
+      if (c < w) pf_e[h] = (g_seg ? lb.eb : near_b)[rs + (g_j0 + c) / NL];
+    }
+  };
+  prefetch_src();
+  // issue the generator's current slice into stage s and advance: the tile as one
+  // bulk copy (lane 0), the coefficients as one 16 B asynchronous copy per lane
+  auto issue = [&](int s) {
+    const int rs = g_seg ? g_rs1 : g_rs, len = g_seg ? g_len1 : g_len;
+    const int w = min(W, len - g_j0);
+    const bool last_seg = g_seg == 1 || g_len1 == 0;
+    const bool first = g_seg == 0 && g_j0 == 0, last = last_seg && g_j0 + w >= len;
+    double* st = ring + s * LY::STAGE;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int c = 2 * lane + 64 * h;
+      if (c < w) ws::cp16_g2s(st + NL * W + c, coef + static_cast<size_t>(pf_e[h]) * NL + (g_j0 + c) % NL);
+    }
+    ws::cp_arrive(bar + s);
+    if (lane == 0) {
+      desc[s] = make_int4(g_e, rs * NL + g_j0, w, (first ? 1 : 0) | (last ? 2 : 0) | (g_seg ? 4 : 0) | ((g_seg && g_j0 == 0) ? 8 : 0));
+      ws::mbar_expect_tx(bar + s, static_cast<unsigned>(w) * NL * 8u);
+      const double* base = (g_seg ? lb.blk : blk) + static_cast<size_t>(rs) * NL * NL;
+      ws::bulk_g2s_hint(st, base + static_cast<size_t>(g_j0) * NL, static_cast<unsigned>(w) * NL * 8u, bar + s, pol);
+    }
+    __syncwarp();
+    g_j0 += w;
+    if (g_j0 >= len) {
+      g_j0 = 0;
+      if (g_seg == 0 && g_len1 > 0) {
+        g_seg = 1;
+      } else {
+        g_e += stride;
+        if (g_e < ne) load_item();
+      }
+    }
+    prefetch_src();
+  };
+  int issued = 0, consumed = 0;
+  for (; issued < NS && g_e < ne; ++issued) issue(issued);
+  double acc[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+  while (consumed < issued) {
+    const int s = consumed % NS;
+    ws::mbar_wait(bar + s, (consumed / NS) & 1);
+    const int4 d = desc[s];
+    const double* st = ring + s * LY::STAGE;
+    if (d.w & 8) {  // first slice of the leaf blocks: this element's coefficients
+      if (lane < NL) xt[lane] = coef[static_cast<size_t>(d.x) * NL + lane];
+      __syncwarp();
+    }
+    if (d.w & 1) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+    }
+    {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {  // columns c, c + 1 of the tile [la][w]: 16 B loads
+        const int c = 2 * lane + 64 * h;
+        if (c < d.z) {
+          const double2 xv = *reinterpret_cast<const double2*>(st + NL * W + c);
+          const double* tc = st + c;
+          if (d.w & 4) {
+            double2 ps = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int la = 0; la < NL; ++la) {
+              const double2 v = *reinterpret_cast<const double2*>(tc + la * d.z);
+              acc[la] = fma(v.x, xv.x, acc[la]);
+              acc[la] = fma(v.y, xv.y, acc[la]);
+              const double t = xt[la];
+              ps.x = fma(v.x, t, ps.x);
+              ps.y = fma(v.y, t, ps.y);
+            }
+            *reinterpret_cast<double2*>(lb.tslot + static_cast<size_t>(d.y) + c) = ps;
+          } else {
+#pragma unroll
+            for (int la = 0; la < NL; ++la) {
+              const double2 v = *reinterpret_cast<const double2*>(tc + la * d.z);
+              acc[la] = fma(v.x, xv.x, acc[la]);
+              acc[la] = fma(v.y, xv.y, acc[la]);
+            }
+          }
+        }
+      }
+    }
+    if (d.w & 2) {  // row sums over the lanes: reduce-scatter, lane l < NL ends with function l
+      col_reduce_rows<NL>(acc, lane);
+      if (lane < NL) rows_out[static_cast<size_t>(d.x) * NL + lane] = acc[0];
+    }
+    __syncwarp();  // every lane is done with stage s (and its descriptor)
+    ++consumed;
+    if (g_e < ne) {  // refill the stage just consumed
+      issue(s);
+      ++issued;
+    }
+  }
 }
 
 // leaf backward transform moments^T down + near rows (h2.cpp:359-371); one
@@ -970,7 +1273,9 @@ template <class S, int NL>
 __global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restrict__ el, int rows, int epp, int npp,
                                                    int leaf_off, const double* __restrict__ mom,
                                                    const S* __restrict__ down, const S* __restrict__ near_rows,
-                                                   S* __restrict__ loc) {
+                                                   S* __restrict__ loc, const int* __restrict__ in_rs = nullptr,
+                                                   const int* __restrict__ in_k = nullptr,
+                                                   const S* __restrict__ tslot = nullptr) {
   pdl_entry();
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(n_el) * NL) return;
@@ -980,6 +1285,8 @@ __global__ void __launch_bounds__(256) k_leaf_down(int n_el, const int* __restri
   const S* dn = down + static_cast<size_t>(leaf) * rows;
   const double* mc = mom + (static_cast<size_t>(e) * NL + l) * rows;
   S acc = zero<S>();
+  if (in_rs != nullptr)  // leaf blocks: transposed products of the pairs (f, e), f < e, in fixed order
+    for (int j = in_rs[e]; j < in_rs[e + 1]; ++j) acc = acc + tslot[static_cast<size_t>(in_k[j]) * NL + l];
   if constexpr (sizeof(S) == 8) {
     // rows even (m^2 nch with m even or nch = 4) and 16 B aligned: paired loads
     if ((rows & 1) == 0) {

@@ -19,7 +19,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libigabem_b200.so")
+# IGB_B200_LIB: another build of the same library (A/B of compile-time variants)
+_LIB_PATH = os.environ.get("IGB_B200_LIB") or os.path.join(_HERE, "libigabem_b200.so")
 _LIB = None
 
 
@@ -91,7 +92,7 @@ SYMBOLS = (
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_create_ex", "igb_plan_counts", "igb_plan_near_pairs",
     "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
     "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
-    "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work", "igb_h2_far_field", "igb_h2_dist_dof_mask",
+    "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work", "igb_h2_leaf_blocks", "igb_h2_far_field", "igb_h2_dist_dof_mask",
 )
 
 
@@ -172,6 +173,7 @@ def lib():
     L.igb_last_error.argtypes = [ctypes.c_char_p, sz]
     L.igb_release_device_memory.argtypes = [i32]
     L.igb_h2_far_work.argtypes = [vp, P(i64)]
+    L.igb_h2_leaf_blocks.argtypes = [vp, P(i64)]
     L.igb_h2_dist_dof_mask.argtypes = [vp, P(ctypes.c_ubyte)]
     L.igb_h2_far_field.argtypes = [vp, P(f64), P(f64), P(f64)]
     L.igb_h2_profile_kernels.argtypes = [vp, i32, i32, ctypes.c_char_p, P(f64), P(i32)]
@@ -630,6 +632,12 @@ class H2Matrix:
         out = np.zeros(2, dtype=np.int64)
         _check(lib().igb_h2_far_work(self._h, _p(out, ctypes.c_longlong)))
         return dict(leaf=int(out[0]), coarse=int(out[1]))
+
+    def leaf_blocks(self):
+        """leaf-level far pairs applied as stored element blocks: (unordered pairs, bytes)"""
+        out = np.zeros(2, dtype=np.int64)
+        _check(lib().igb_h2_leaf_blocks(self._h, _p(out, ctypes.c_longlong)))
+        return int(out[0]), int(out[1])
 
     def bench_steps(self, steps, matvecs):
         """steps x (device assembly + matvecs matvecs): (total ms, assembly ms) from CUDA events."""
