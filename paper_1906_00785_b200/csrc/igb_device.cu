@@ -176,10 +176,10 @@ T* H2Device::upload(const std::vector<T>& v) {
 }
 
 // default fraction of each leaf target's upper far pairs applied as stored
-// element blocks (IGB_H2_LEAF_BLOCKS overrides): warp-specialised leaf kernel
-// (c5: leaf kernel 7.38 ms without blocks, 6.14 / 5.84 / 5.81 ms at 0.4 / 0.5 /
-// 0.6) and the one-warp-per-target fused kernel (c5: 7.30 -> 6.71 ms at 0.4)
-constexpr double kLeafBlockFractionWs = 0.5, kLeafBlockFraction = 0.4;
+// element blocks (IGB_H2_LEAF_BLOCKS overrides): warp-specialised kernel (c5
+// matvec 10.02 / 9.77 / 9.57 / 9.53 ms at 0.5 / 0.6 / 0.7 / 0.8; 10.88 ms before)
+// and the one-warp-per-target fused kernel (c5 leaf kernel 7.30 -> 6.71 ms at 0.4)
+constexpr double kLeafBlockFractionWs = 0.75, kLeafBlockFraction = 0.4;
 // IGB_H2_LEAF_WS=0: the one-warp-per-target fused leaf kernel instead of k_leaf_ws
 static bool leaf_ws_enabled() {
   const char* e = getenv("IGB_H2_LEAF_WS");
@@ -512,6 +512,11 @@ void H2Device::stage_plan() {
       for (int t : coarse) sym_pairs_[1] += P.far_row_start[t + 1] - P.far_upper_start[t];
       d_sym_fine_ = upload(fine);
       d_sym_coarse_ = upload(coarse);
+      {  // k_leaf_ws takes every target: the coarse levels first
+        std::vector<int> all(coarse);
+        all.insert(all.end(), fine.begin(), fine.end());
+        d_sym_all_ = upload(all);
+      }
       // fused leaf far field + near rows (single GPU, m = 4): the elements whose
       // leaf has no upper far pairs get near-only warps
       bool ident = Lp.world == 1 && static_cast<int>(Lp.el.size()) == d.element_count();
@@ -548,14 +553,13 @@ void H2Device::stage_plan() {
         }
         if (frac > 0.0 && lb_rs[ne] > 0) {
           const int nb = lb_rs[ne];
-          std::vector<int> nt(nb), ns(nb), eb(nb), in_rs(ne + 1, 0), in_k(nb);
+          std::vector<int> ns(nb), eb(nb), in_rs(ne + 1, 0), in_k(nb);
 #pragma omp parallel for schedule(static)
           for (int e = 0; e < ne; ++e) {
             const int t = leaf_of(e), cnt = lb_rs[e + 1] - lb_rs[e];
             upper_end[t] -= cnt;
             for (int k = 0; k < cnt; ++k) {
               const int sq = P.far_b[upper_end[t] + k];
-              nt[lb_rs[e] + k] = t;
               ns[lb_rs[e] + k] = sq;
               eb[lb_rs[e] + k] = (sq / P.npp) * epp + (sq % P.npp - leaf_off);
             }
@@ -572,7 +576,6 @@ void H2Device::stage_plan() {
           d_upper_end_ = upload(upper_end);
           d_lb_rs_ = upload(lb_rs);
           d_lb_eb_ = upload(eb);
-          d_lb_nt_ = upload(nt);
           d_lb_ns_ = upload(ns);
           d_lb_in_rs_ = upload(in_rs);
           d_lb_in_k_ = upload(in_k);
@@ -704,15 +707,12 @@ void H2Device::launch_plan_phase(cudaEvent_t* ev, int& launched) {
   }
   if (n_leaf_blocks_ > 0) {
     if constexpr (KT::KIND == 0 && NL <= 16) {
-      const int nb = static_cast<int>(n_leaf_blocks_);
-      auto go = [&](auto kern, int M_) {
-        const size_t smem = 4 * static_cast<size_t>(2 * NL * M_ * M_ + M_ * M_ * M_ * M_ + M_ * M_ * NL + 6 * M_ * M_) * 8;
-        IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<grid_for(nb, 4), 128, smem, stream_>>>(nb, d_lb_nt_, d_lb_ns_, d_lb_rs_, d.elements_per_patch(), P.npp,
-                                                      P.level_offset[P.depth], d_img_, d_mom_, d_lb_blk_);
+      auto go = [&](auto kern) {
+        kern<<<d.element_count(), 128, 0, stream_>>>(d.element_count(), d_lb_rs_, d_lb_ns_, d.elements_per_patch(), P.npp,
+                                                     P.level_offset[P.depth], d_img_, d_mom_, d_lb_blk_);
       };
-      if (m == 4) go(k_leaf_blocks<4, NL>, 4);
-      else go(k_leaf_blocks<5, NL>, 5);
+      if (m == 4) go(k_leaf_blocks<4, NL>);
+      else go(k_leaf_blocks<5, NL>);
       ++launched;
       IGB_CUDA(cudaGetLastError());
     }
@@ -1105,7 +1105,7 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
       static_cast<S*>(leaf_ws ? coef : nullptr));
   ++launches;
   tick("leaf_up");
-  if (!prof) {
+  if (!prof && !leaf_ws) {
     IGB_CUDA(cudaEventRecord(ev_fork2_, s));
     IGB_CUDA(cudaStreamWaitEvent(side2_, ev_fork2_, 0));
   }
@@ -1136,6 +1136,57 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
         P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn, which, npp, P.level_offset[L]);
     ++launches;
   };
+  if (leaf_ws) {
+    // one stream: upward pass, then k_leaf_ws -- its far warps evaluate the far
+    // field of every level (coarse targets first) while its stream warps move the
+    // near rows and leaf blocks --, slot sums, downward pass, leaf transform
+    if constexpr (KT::KIND == 0 && NL == 16) {
+      for (int l = L - 1; l >= 0; --l) {
+        const long long tot = (l == 0 ? static_cast<long long>(np) : static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * (l - 1)))) * rows;
+        launch_up_level<S>(grid_for(tot, 256), s, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                           d_tl_, d_tr_, up, l == 0 ? 0 : Lp.c0, l == 0 ? 0 : Lp.c1);
+        ++launches;
+      }
+      tick("upward");
+      LeafBlocks lbk{far_end, nullptr, nullptr, nullptr, nullptr};
+      if (blocks) lbk = LeafBlocks{d_upper_end_, d_lb_rs_, d_lb_eb_, d_lb_blk_, d_lb_tslot_};
+      auto ws_launch = [&](auto kern, size_t smem) {
+        int nsm = 0;
+        IGB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_));
+        IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<nsm, 32 * (ws::kFarWarps + ws::kStreamWarps), smem, s>>>(
+            n_sym_coarse_ + n_sym_fine_, d_sym_all_, d.element_count(), d_upper_start_, lbk, d_far_b_, d_trans_, d_img_,
+            upd, dn, d_slot_, d_near_rs_, d_near_b_, reinterpret_cast<const double*>(d_near_),
+            reinterpret_cast<const double*>(coef), reinterpret_cast<double*>(nrows));
+      };
+      if (m == 4) ws_launch(k_leaf_ws<4, NL, 2>, ws::Layout<4, NL>::BYTES);
+      else ws_launch(k_leaf_ws<5, NL, 2>, ws::Layout<5, NL>::BYTES);
+      ++launches;
+      tick("far_near");
+      far_lower(s, 0);
+      tick("far_lower");
+      if (!prof) IGB_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+      if (far_only_) return;  // introspection: stop after the far field (phase 4)
+      for (int l = 0; l < L; ++l) {
+        const long long tot = static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * l)) * rows;
+        launch_down_level<S>(grid_for(tot, 256), s, np, l, npp, P.level_offset[l], P.level_offset[l + 1], m, nch_,
+                             d_tl_, d_tr_, down, Lp.c0, Lp.c1);
+        ++launches;
+      }
+      tick("downward");
+      pdl_launch(k_leaf_down<S, NL>, grid_for(static_cast<long long>(nel) * NL, 256), 256, 0, s,
+          nel, d_el_, rows, epp, npp, P.level_offset[L], d_mom_, down, nrows, loc,
+          static_cast<const int*>(blocks ? d_lb_in_rs_ : nullptr), static_cast<const int*>(blocks ? d_lb_in_k_ : nullptr),
+          blocks ? reinterpret_cast<const S*>(d_lb_tslot_) : static_cast<const S*>(nullptr));
+      tick("leaf_down");
+      pdl_launch(k_scatter<S>, grid_for(d.dof_count(), 256), 256, 0, s, d.dof_count(), d_dof_start_, d_dof_inc_, d_loc_sign_, loc, y);
+      launches += 2;
+      tick("scatter");
+      IGB_CUDA(cudaGetLastError());
+      apply_launches_ = launches;
+    }
+    return;
+  }
   // side stream 2: upward pass, coarse far field, downward levels 0 .. L-2
   for (int l = L - 1; l >= 0; --l) {
     const long long tot = (l == 0 ? static_cast<long long>(np) : static_cast<long long>(Lp.c1 - Lp.c0) * (1LL << (2 * (l - 1)))) * rows;
@@ -1169,23 +1220,7 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
             reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(x),
             reinterpret_cast<double*>(nrows), d_l2g_, d_lsign_);
       };
-      if constexpr (NL == 16) {
-        if (leaf_ws) {
-          auto ws_launch = [&](auto kern, size_t smem) {
-            int nsm = 0;
-            IGB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_));
-            IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            kern<<<nsm, 32 * (ws::kFarWarps + ws::kStreamWarps), smem, s>>>(
-                n_sym_fine_, d_sym_fine_, d.element_count(), d_upper_start_, lbk, d_far_b_, d_trans_, d_img_, upd, dn,
-                d_slot_, d_near_rs_, d_near_b_, reinterpret_cast<const double*>(d_near_),
-                reinterpret_cast<const double*>(coef), reinterpret_cast<double*>(nrows));
-          };
-          if (m == 4) ws_launch(k_leaf_ws<4, NL, 2>, ws::Layout<4, NL>::BYTES);
-          else ws_launch(k_leaf_ws<5, NL, 2>, ws::Layout<5, NL>::BYTES);
-        }
-      }
-      if (leaf_ws) {
-      } else if (m == 4)
+      if (m == 4)
         fused_launch(k_far_col_near<4, NL, 3, 2>);
       else
         fused_launch(k_far_col_near<5, NL, 2, 2>);

@@ -160,7 +160,7 @@ class H2Device {
   int *d_col_rs_ = nullptr, *d_col_q_ = nullptr;  // multi-GPU ranks: per-target pair lists (k_far_col_list)
   int n_sym_fine_ = 0, n_sym_coarse_ = 0;  // leaf-level / coarser symmetric targets
   long long sym_pairs_[2] = {0, 0};        // unordered far pairs evaluated by them
-  int *d_sym_fine_ = nullptr, *d_sym_coarse_ = nullptr;
+  int *d_sym_fine_ = nullptr, *d_sym_coarse_ = nullptr, *d_sym_all_ = nullptr;
   int n_near_rest_ = -1;  // fused leaf far field + near rows: elements without leaf targets (-1: off)
   int* d_near_rest_ = nullptr;
   double* d_slot_ = nullptr;
@@ -169,7 +169,7 @@ class H2Device {
   // elements, blocks in the block-row layout, transposed products
   long long n_leaf_blocks_ = 0;
   size_t leaf_block_bytes_ = 0;
-  int *d_upper_end_ = nullptr, *d_lb_rs_ = nullptr, *d_lb_eb_ = nullptr, *d_lb_nt_ = nullptr, *d_lb_ns_ = nullptr;
+  int *d_upper_end_ = nullptr, *d_lb_rs_ = nullptr, *d_lb_eb_ = nullptr, *d_lb_ns_ = nullptr;
   int *d_lb_in_rs_ = nullptr, *d_lb_in_k_ = nullptr;
   double *d_lb_blk_ = nullptr, *d_lb_tslot_ = nullptr;
   int *d_far_a_ = nullptr;

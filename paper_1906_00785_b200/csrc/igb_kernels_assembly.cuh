@@ -158,59 +158,53 @@ __global__ void __launch_bounds__(256) k_couplings(long long n_pairs, int mm, co
 //   B[la][lb] = sum_nu sum_mu mom_t[la][nu] K[nu][mu] mom_s[lb][mu],
 // K[nu][mu] = G(|img_t[nu] - img_s[mu]|) -- what apply() computes for the pair
 // through leaf moments, coupling and leaf transform (h2.cpp:281-290, 312-326,
-// 359-371), assembled once.  Written into the row of element t in the tiled
-// block-row layout (row_tile_off; k: position among the row's blocked pairs).  One
-// warp per pair, four per CTA.
+// 359-371), assembled once.  One CTA per test element t: its moments stay in
+// shared memory while the CTA walks the row's blocked pairs (K, then
+// T = K mom_s^T, then B = mom_t T) and writes them into the row in the tiled
+// block-row layout (row_tile_off; k: position among the row's blocked pairs).
 template <int M, int NL>
-__global__ void __launch_bounds__(128) k_leaf_blocks(int n_pairs, const int* __restrict__ node_t,
-                                                     const int* __restrict__ node_s, const int* __restrict__ rs,
-                                                     int epp, int npp, int leaf_off, const double* __restrict__ img,
-                                                     const double* __restrict__ mom, double* __restrict__ blk) {
+__global__ void __launch_bounds__(128) k_leaf_blocks(int ne, const int* __restrict__ rs,
+                                                     const int* __restrict__ node_s, int epp, int npp, int leaf_off,
+                                                     const double* __restrict__ img, const double* __restrict__ mom,
+                                                     double* __restrict__ blk) {
   constexpr int MM = M * M;
-  constexpr int PER = 2 * NL * MM + MM * MM + MM * NL + 6 * MM;  // Mt, Ms, K, T, images
-  extern __shared__ __align__(16) double lbsm[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k = blockIdx.x * 4 + w;
-  if (k >= n_pairs) return;
-  double* Mt = lbsm + static_cast<size_t>(w) * PER;
-  double* Ms = Mt + NL * MM;
-  double* K = Ms + NL * MM;
-  double* T = K + MM * MM;
-  double* it = T + MM * NL;
-  double* is = it + 3 * MM;
-  const int t = node_t[k], s = node_s[k];
-  const int et = (t / npp) * epp + (t % npp - leaf_off), es = (s / npp) * epp + (s % npp - leaf_off);
-  for (int i = lane; i < NL * MM; i += 32) {
-    Mt[i] = __ldg(mom + static_cast<size_t>(et) * NL * MM + i);
-    Ms[i] = __ldg(mom + static_cast<size_t>(es) * NL * MM + i);
-  }
-  for (int i = lane; i < 3 * MM; i += 32) {
-    it[i] = __ldg(img + static_cast<size_t>(t) * 3 * MM + i);
-    is[i] = __ldg(img + static_cast<size_t>(s) * 3 * MM + i);
-  }
-  __syncwarp();
-  for (int i = lane; i < MM * MM; i += 32) {
-    const int nu = i / MM, mu = i - nu * MM;
-    const double d0 = it[3 * nu] - is[3 * mu], d1 = it[3 * nu + 1] - is[3 * mu + 1], d2 = it[3 * nu + 2] - is[3 * mu + 2];
-    K[i] = kInv4Pi / sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-  }
-  __syncwarp();
-  for (int i = lane; i < MM * NL; i += 32) {  // T[nu][lb] = sum_mu K[nu][mu] Ms[lb][mu]
-    const int nu = i / NL, lb = i - nu * NL;
-    double a = 0.0;
-#pragma unroll 5
-    for (int mu = 0; mu < MM; ++mu) a = fma(K[nu * MM + mu], Ms[lb * MM + mu], a);
-    T[i] = a;
-  }
-  __syncwarp();
-  const int r0 = rs[et], cnt = rs[et + 1] - r0, kk = k - r0;
+  __shared__ double Mt[NL * MM], Ms[NL * MM], K[MM * MM], T[MM * NL], it[3 * MM], is[3 * MM];
+  const int e = blockIdx.x, tid = threadIdx.x;
+  if (e >= ne) return;
+  const int r0 = rs[e], cnt = rs[e + 1] - r0;
+  if (cnt == 0) return;
+  const int t = (e / epp) * npp + leaf_off + e % epp;
+  for (int i = tid; i < NL * MM; i += 128) Mt[i] = __ldg(mom + static_cast<size_t>(e) * NL * MM + i);
+  for (int i = tid; i < 3 * MM; i += 128) it[i] = __ldg(img + static_cast<size_t>(t) * 3 * MM + i);
   double* out = blk + static_cast<size_t>(r0) * NL * NL;
-  for (int i = lane; i < NL * NL; i += 32) {  // B[la][lb] = sum_nu Mt[la][nu] T[nu][lb]
-    const int la = i / NL, lb = i - la * NL;
-    double a = 0.0;
+  for (int kk = 0; kk < cnt; ++kk) {
+    const int s = node_s[r0 + kk];
+    const int es = (s / npp) * epp + (s % npp - leaf_off);
+    __syncthreads();  // the previous pair is done with Ms, is, T
+    for (int i = tid; i < NL * MM; i += 128) Ms[i] = __ldg(mom + static_cast<size_t>(es) * NL * MM + i);
+    for (int i = tid; i < 3 * MM; i += 128) is[i] = __ldg(img + static_cast<size_t>(s) * 3 * MM + i);
+    __syncthreads();
+    for (int i = tid; i < MM * MM; i += 128) {
+      const int nu = i / MM, mu = i - nu * MM;
+      const double d0 = it[3 * nu] - is[3 * mu], d1 = it[3 * nu + 1] - is[3 * mu + 1], d2 = it[3 * nu + 2] - is[3 * mu + 2];
+      K[i] = kInv4Pi * rsqrt_nr(d0 * d0 + d1 * d1 + d2 * d2);
+    }
+    __syncthreads();
+    for (int i = tid; i < MM * NL; i += 128) {  // T[nu][lb] = sum_mu K[nu][mu] Ms[lb][mu]
+      const int nu = i / NL, lb = i - nu * NL;
+      double a = 0.0;
 #pragma unroll 5
-    for (int nu = 0; nu < MM; ++nu) a = fma(Mt[la * MM + nu], T[nu * NL + lb], a);
-    out[row_tile_off(cnt * NL, NL, la, kk * NL + lb)] = a;
+      for (int mu = 0; mu < MM; ++mu) a = fma(K[nu * MM + mu], Ms[lb * MM + mu], a);
+      T[i] = a;
+    }
+    __syncthreads();
+    for (int i = tid; i < NL * NL; i += 128) {  // B[la][lb] = sum_nu Mt[la][nu] T[nu][lb]
+      const int la = i / NL, lb = i - la * NL;
+      double a = 0.0;
+#pragma unroll 5
+      for (int nu = 0; nu < MM; ++nu) a = fma(Mt[la * MM + nu], T[nu * NL + lb], a);
+      out[row_tile_off(cnt * NL, NL, la, kk * NL + lb)] = a;
+    }
   }
 }
 

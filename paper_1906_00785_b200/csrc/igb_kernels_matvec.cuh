@@ -50,13 +50,15 @@ __global__ void k_leaf_up_x(int n_el, int rows, int epp, int npp, int leaf_off, 
   if (idx < ndown) down[idx] = zero<S>();
   if (idx >= static_cast<long long>(n_el) * rows) return;
   const int e = static_cast<int>(idx / rows), r = static_cast<int>(idx % rows);
-  if (coef_out != nullptr && r < NL) coef_out[e * NL + r] = x[l2g[e * NL + r]] * sg[e * NL + r];  // rows >= NL
-  S acc = zero<S>();
+  S acc = zero<S>(), mine = zero<S>();
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
     const int k = e * NL + l;
-    fmac(acc, x[l2g[k]] * sg[k], __ldg(mom + static_cast<size_t>(k) * rows + r));
+    const S c = x[l2g[k]] * sg[k];
+    if (l == r) mine = c;
+    fmac(acc, c, __ldg(mom + static_cast<size_t>(k) * rows + r));
   }
+  if (coef_out != nullptr && r < NL) coef_out[e * NL + r] = mine;  // rows >= NL
   const int leaf = (e / epp) * npp + leaf_off + (e % epp);
   up[static_cast<size_t>(leaf) * rows + r] = acc;
 }
