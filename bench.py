@@ -311,7 +311,7 @@ def kernel_rooflines(h, c, disc, prof, iters, peaks, src, traffic):
                     "unit": "TFLOP/s", "peak_source": "measured DFMA probe (profiles/r01_fp64_peak_probe.txt)",
                     "flops_per_launch": fl, "kernel_evals": evals, "ms": ms, "note": note}
 
-    blk_pairs, blk_bytes = h.leaf_blocks()
+    blk_pairs, blk_bytes, stream_bytes = h.leaf_blocks()
     if "far_near" in prof:  # k_leaf_ws: far field of every level + near rows + leaf blocks in one launch
         ms = prof["far_near"] / iters
         fp64("far_near", (sym["leaf"] + sym["coarse"]) * mm * mm, ms,
@@ -319,8 +319,8 @@ def kernel_rooflines(h, c, disc, prof, iters, peaks, src, traffic):
              "(m^4 evaluations each), stream warps move the near rows and the leaf blocks (bulk copies)")
         r = out["far_near"]
         r["fp64_frac"] = r["achieved"] / r["peak"]
-        r["hbm_bytes_per_launch"] = near_bytes + blk_bytes
-        r["hbm_achieved_gbs"] = (near_bytes + blk_bytes) / (ms * 1e-3) / 1e9
+        r["hbm_bytes_per_launch"] = stream_bytes  # block rows: near field (once per unordered pair) + leaf blocks
+        r["hbm_achieved_gbs"] = stream_bytes / (ms * 1e-3) / 1e9
         r["hbm_frac"] = r["hbm_achieved_gbs"] / hbm
         r["leaf_block_pairs"] = blk_pairs
         if r["hbm_frac"] > r["fp64_frac"]:  # report the roofline the kernel sits closer to

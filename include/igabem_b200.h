@@ -181,10 +181,12 @@ int igb_h2_far_work(const igb_h2* h, long long pairs[2]);
 /* leaf blocks: leaf-level admissible pairs the matvec applies as stored element
  * blocks M_t K M_s^T (what apply() computes for the pair, h2.cpp:281-290 /
  * 312-326 / 359-371, assembled once) instead of evaluating their couplings:
- * out[0] = unordered pairs, out[1] = bytes of their blocks (0, 0: none).  The
- * environment variable IGB_H2_LEAF_BLOCKS (fraction of every leaf target's
- * pairs, 0 disables) is read at construction. */
-int igb_h2_leaf_blocks(const igb_h2* h, long long out[2]);
+ * out[0] = unordered pairs, out[1] = bytes of their blocks (0, 0: none),
+ * out[2] = bytes of block rows (near field + leaf blocks) one matvec streams --
+ * the warp-specialised leaf kernel also stores the near field once per
+ * unordered pair.  The environment variable IGB_H2_LEAF_BLOCKS (fraction of
+ * every leaf target's pairs, 0 disables) is read at construction. */
+int igb_h2_leaf_blocks(const igb_h2* h, long long out[3]);
 /* introspection of the far field (phase 4 of H2Matrix::apply, h2.cpp:312-326):
  * runs the matvec on host x through the upward pass and the far field (with
  * the kernel the matvec uses), then copies up and down, each

@@ -442,12 +442,13 @@ int igb_h2_far_work(const igb_h2* h, long long pairs[2]) {
     pairs[1] = h->dev->sym_pairs(1);
   });
 }
-int igb_h2_leaf_blocks(const igb_h2* h, long long out[2]) {
+int igb_h2_leaf_blocks(const igb_h2* h, long long out[3]) {
   return guard([&] {
     need(h, "h2");
     need(out, "out");
     out[0] = h->dev->leaf_block_pairs();
     out[1] = static_cast<long long>(h->dev->leaf_block_bytes());
+    out[2] = static_cast<long long>(h->dev->block_stream_bytes());
   });
 }
 int igb_h2_profile_apply(igb_h2* h, int iters, double phase_ms[8]) {

@@ -104,6 +104,19 @@ static cudaMemPool_t device_pool(int device) {
   return pool;
 }
 
+// device memory an operator can still take: what the driver reports free plus
+// what the per-device pool holds but does not use (memory of destroyed
+// operators stays reserved there)
+static size_t available_device_bytes(int device) {
+  size_t free_b = 0, total_b = 0;
+  IGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  uint64_t reserved = 0, used = 0;
+  cudaMemPool_t pool = device_pool(device);
+  IGB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  IGB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  return free_b + static_cast<size_t>(reserved > used ? reserved - used : 0);
+}
+
 void release_device_memory(int device) {
   cudaMemPool_t pool = device_pool(device);
   IGB_CUDA(cudaSetDevice(device));
@@ -179,7 +192,7 @@ T* H2Device::upload(const std::vector<T>& v) {
 // element blocks (IGB_H2_LEAF_BLOCKS overrides): warp-specialised kernel (c5
 // matvec 10.02 / 9.77 / 9.57 / 9.53 ms at 0.5 / 0.6 / 0.7 / 0.8; 10.88 ms before)
 // and the one-warp-per-target fused kernel (c5 leaf kernel 7.30 -> 6.71 ms at 0.4)
-constexpr double kLeafBlockFractionWs = 0.75, kLeafBlockFraction = 0.4;
+constexpr double kLeafBlockFractionWs = 0.9, kLeafBlockFraction = 0.4;
 // IGB_H2_LEAF_WS=0: the one-warp-per-target fused leaf kernel instead of k_leaf_ws
 static bool leaf_ws_enabled() {
   const char* e = getenv("IGB_H2_LEAF_WS");
@@ -288,8 +301,7 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   // (c4: 6.2 ms per matvec stored at 93 % of HBM vs 14.6 ms evaluated); Laplace
   // always evaluates them (c5: the symmetric FP64 kernel beats the 161 GB stream)
   if (!(flags_ & (kStoredCouplings | kFusedCouplings)) && opt_.world == 1 && d.is_complex()) {
-    size_t free_b = 0, total_b = 0;
-    IGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = available_device_bytes(device_);
     const size_t mm = static_cast<size_t>(opt_.m) * opt_.m;
     if (plan_.far_a.size() * mm * mm * 16 <= free_b / 2) flags_ |= kStoredCouplings;
   }
@@ -540,47 +552,100 @@ void H2Device::stage_plan() {
         frac = std::min(1.0, std::max(0.0, frac));
         const int ne = d.element_count(), leaf_off = P.level_offset[P.depth];
         auto leaf_of = [&](int e) { return (e / epp) * P.npp + leaf_off + e % epp; };
+        // warp-specialised kernel: the near field joins the block rows, stored once
+        // per unordered pair as well -- row e = [near blocks (e, f), f >= e, the
+        // diagonal block halved][blocked far pairs]; k_pack_sym_near copies them from
+        // the near storage -- so its stream warps move half the near bytes
+        const bool sym_near = NL == 16 && leaf_ws_enabled() && (m == 4 || m == 5) && frac > 0.0;
+        const auto t_lb = std::chrono::steady_clock::now();
+        auto lb_lap = [&](const char* what) {
+          if (getenv("IGB_VERBOSE"))
+            fprintf(stderr, "[igb ctor] leaf blocks: %-12s %8.2f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_lb).count());
+        };
         std::vector<int> lb_rs(ne + 1, 0), upper_end(P.far_row_start.begin() + 1, P.far_row_start.end());
+        std::vector<int> n_sym(ne, 0), n_far(ne, 0);
+        for (int e = 0; e < ne && sym_near; ++e) {
+          const auto first = P.near_b.begin() + P.near_row_start[e], last = P.near_b.begin() + P.near_row_start[e + 1];
+          n_sym[e] = static_cast<int>(last - std::lower_bound(first, last, e));
+        }
+        long long n_far_total = 0;
         for (; frac > 0.0; frac *= 0.5) {  // within a quarter of the free device memory
+          n_far_total = 0;
           for (int e = 0; e < ne; ++e) {
             const int t = leaf_of(e), nup = P.far_row_start[t + 1] - P.far_upper_start[t];
-            lb_rs[e + 1] = lb_rs[e] + std::min(nup, static_cast<int>(frac * nup + 0.5));
+            n_far[e] = std::min(nup, static_cast<int>(frac * nup + 0.5));
+            n_far_total += n_far[e];
+            lb_rs[e + 1] = lb_rs[e] + n_sym[e] + n_far[e];
           }
-          size_t free_b = 0, total_b = 0;
-          IGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+          const size_t free_b = available_device_bytes(device_);
           const size_t fixed = (static_cast<size_t>(Lp.near_row.size()) * NL * NL + P.far_a.size() * mm) * 8;
           if (static_cast<double>(lb_rs[ne]) * NL * NL * 8 <= 0.25 * (static_cast<double>(free_b) - fixed)) break;
         }
-        if (frac > 0.0 && lb_rs[ne] > 0) {
+        lb_lap("counts");
+        if (frac > 0.0 && n_far_total > 0) {
           const int nb = lb_rs[ne];
-          std::vector<int> ns(nb), eb(nb), in_rs(ne + 1, 0), in_k(nb);
+          // per position: source element, far node (-1: near block), near slot (-1: far pair)
+          std::vector<int> ns(nb, -1), eb(nb), nq(nb, -1), in_rs(ne + 1, 0), in_k(nb);
 #pragma omp parallel for schedule(static)
           for (int e = 0; e < ne; ++e) {
-            const int t = leaf_of(e), cnt = lb_rs[e + 1] - lb_rs[e];
-            upper_end[t] -= cnt;
-            for (int k = 0; k < cnt; ++k) {
-              const int sq = P.far_b[upper_end[t] + k];
-              ns[lb_rs[e] + k] = sq;
-              eb[lb_rs[e] + k] = (sq / P.npp) * epp + (sq % P.npp - leaf_off);
+            const int t = leaf_of(e);
+            int k = lb_rs[e];
+            for (int q = P.near_row_start[e + 1] - n_sym[e]; q < P.near_row_start[e + 1]; ++q, ++k) {
+              eb[k] = P.near_b[q];
+              nq[k] = q;
+            }
+            upper_end[t] -= n_far[e];
+            for (int j = 0; j < n_far[e]; ++j, ++k) {
+              const int sq = P.far_b[upper_end[t] + j];
+              ns[k] = sq;
+              eb[k] = (sq / P.npp) * epp + (sq % P.npp - leaf_off);
             }
           }
+          lb_lap("positions");
           for (int k = 0; k < nb; ++k) ++in_rs[eb[k] + 1];
           for (int e = 0; e < ne; ++e) in_rs[e + 1] += in_rs[e];
           {
             std::vector<int> fill(in_rs.begin(), in_rs.end() - 1);
             for (int k = 0; k < nb; ++k) in_k[fill[eb[k]]++] = k;  // ascending k: fixed summation order
           }
-          n_leaf_blocks_ = nb;
-          leaf_block_bytes_ = static_cast<size_t>(nb) * NL * NL * 8;
-          sym_pairs_[0] -= nb;
+          lb_lap("in lists");
+          n_leaf_blocks_ = n_far_total;
+          leaf_block_bytes_ = static_cast<size_t>(n_far_total) * NL * NL * 8;
+          n_lb_total_ = nb;
+          lb_sym_near_ = sym_near;
+          sym_pairs_[0] -= n_far_total;
+          {  // slots the far kernels write: per row s the pairs (s, t), t < s, that t evaluates
+            std::vector<int> low_rs(P.n_nodes + 1, 0);
+#pragma omp parallel for schedule(static)
+            for (int sn = 0; sn < P.n_nodes; ++sn) {
+              int c = 0;
+              for (int q = P.far_row_start[sn]; q < P.far_upper_start[sn]; ++q)
+                c += P.far_trans[q] < upper_end[P.far_b[q]];
+              low_rs[sn + 1] = c;
+            }
+            for (int sn = 0; sn < P.n_nodes; ++sn) low_rs[sn + 1] += low_rs[sn];
+            std::vector<int> low_q(low_rs[P.n_nodes]);
+#pragma omp parallel for schedule(static)
+            for (int sn = 0; sn < P.n_nodes; ++sn) {
+              int k = low_rs[sn];
+              for (int q = P.far_row_start[sn]; q < P.far_upper_start[sn]; ++q)
+                if (P.far_trans[q] < upper_end[P.far_b[q]]) low_q[k++] = q;
+            }
+            d_low_rs_ = upload(low_rs);
+            d_low_q_ = upload(low_q);
+          }
+          lb_lap("slot lists");
           d_upper_end_ = upload(upper_end);
           d_lb_rs_ = upload(lb_rs);
           d_lb_eb_ = upload(eb);
           d_lb_ns_ = upload(ns);
+          if (sym_near) d_lb_nq_ = upload(nq);
           d_lb_in_rs_ = upload(in_rs);
           d_lb_in_k_ = upload(in_k);
           d_lb_blk_ = dalloc<double>(static_cast<size_t>(nb) * NL * NL);
           d_lb_tslot_ = dalloc<double>(static_cast<size_t>(nb) * NL);
+          lb_lap("uploads");
         }
       }
       if (Lp.world > 1 && sym_far_ && m <= 5) {  // per-target column lists for k_far_col_list
@@ -745,6 +810,14 @@ void H2Device::launch_plan_phase(cudaEvent_t* ev, int& launched) {
         reinterpret_cast<S*>(d_near_));
     ++launched;
     IGB_CUDA(cudaGetLastError());
+  }
+  if (lb_sym_near_) {  // the near blocks (e, f), f >= e, into the block rows of k_leaf_ws
+    if constexpr (KT::KIND == 0 && NL == 16) {
+      k_pack_sym_near<NL><<<grid_for(static_cast<long long>(n_lb_total_) * 32, 128), 128, 0, stream_>>>(
+          n_lb_total_, d_lb_nq_, d_lb_eb_, d_lb_rs_, d_near_a_, d_near_rs_, d_near_, d_lb_blk_);
+      ++launched;
+      IGB_CUDA(cudaGetLastError());
+    }
   }
   IGB_CUDA(cudaEventRecord(ev[kEvScatter], stream_));
 }
@@ -1132,6 +1205,13 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
     ++launches;
   };
   auto far_lower = [&](cudaStream_t st, int which) {
+    if (blocks) {  // only the slots the far kernels wrote (the blocked pairs have none)
+      pdl_launch(k_far_lower_list, grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, st,
+          P.n_nodes, mm, static_cast<const int*>(d_low_rs_), static_cast<const int*>(d_low_q_),
+          static_cast<const double*>(d_slot_), dn, which, npp, P.level_offset[L]);
+      ++launches;
+      return;
+    }
     pdl_launch(k_far_lower<false>, grid_for(static_cast<long long>(P.n_nodes) * mm, 256), 256, 0, st, 
         P.n_nodes, mm, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, dn, which, npp, P.level_offset[L]);
     ++launches;
@@ -1156,8 +1236,9 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
         IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<nsm, 32 * (ws::kFarWarps + ws::kStreamWarps), smem, s>>>(
             n_sym_coarse_ + n_sym_fine_, d_sym_all_, d.element_count(), d_upper_start_, lbk, d_far_b_, d_trans_, d_img_,
-            upd, dn, d_slot_, d_near_rs_, d_near_b_, reinterpret_cast<const double*>(d_near_),
-            reinterpret_cast<const double*>(coef), reinterpret_cast<double*>(nrows));
+            upd, dn, d_slot_, (blocks && lb_sym_near_) ? nullptr : d_near_rs_, d_near_b_,
+            reinterpret_cast<const double*>(d_near_), reinterpret_cast<const double*>(coef),
+            reinterpret_cast<double*>(nrows));
       };
       if (m == 4) ws_launch(k_leaf_ws<4, NL, 2>, ws::Layout<4, NL>::BYTES);
       else ws_launch(k_leaf_ws<5, NL, 2>, ws::Layout<5, NL>::BYTES);

@@ -81,6 +81,11 @@ class H2Device {
   // leaf-level far pairs applied as stored element blocks (LeafBlocks) and their bytes
   long long leaf_block_pairs() const { return n_leaf_blocks_; }
   size_t leaf_block_bytes() const { return leaf_block_bytes_; }
+  // bytes of block rows one matvec streams (near field + leaf blocks as the leaf kernel reads them)
+  size_t block_stream_bytes() const {
+    const size_t nl2 = static_cast<size_t>(disc_->local_count()) * disc_->local_count() * (is_complex() ? 16 : 8);
+    return lb_sym_near_ ? static_cast<size_t>(n_lb_total_) * nl2 : bytes_.near + leaf_block_bytes_;
+  }
   // `steps` x (device assembly + `matvecs` matvecs), CUDA events; returns ms
   double bench_steps(int steps, int matvecs, double* assembly_ms);
   int assembly_kernel_launches() const { return assembly_kernels_; }
@@ -169,6 +174,10 @@ class H2Device {
   // elements, blocks in the block-row layout, transposed products
   long long n_leaf_blocks_ = 0;
   size_t leaf_block_bytes_ = 0;
+  int n_lb_total_ = 0;        // block-row positions: blocked far pairs (+ near pairs f >= e when lb_sym_near_)
+  bool lb_sym_near_ = false;  // k_leaf_ws: the near field is part of the block rows (stored once per unordered pair)
+  int* d_lb_nq_ = nullptr;
+  int *d_low_rs_ = nullptr, *d_low_q_ = nullptr;  // per node: the lower pairs whose slots are written
   int *d_upper_end_ = nullptr, *d_lb_rs_ = nullptr, *d_lb_eb_ = nullptr, *d_lb_ns_ = nullptr;
   int *d_lb_in_rs_ = nullptr, *d_lb_in_k_ = nullptr;
   double *d_lb_blk_ = nullptr, *d_lb_tslot_ = nullptr;

@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(128) k_leaf_blocks(int ne, const int* __restri
   double* out = blk + static_cast<size_t>(r0) * NL * NL;
   for (int kk = 0; kk < cnt; ++kk) {
     const int s = node_s[r0 + kk];
+    if (s < 0) continue;  // a near block of the row (k_pack_sym_near)
     const int es = (s / npp) * epp + (s % npp - leaf_off);
     __syncthreads();  // the previous pair is done with Ms, is, T
     for (int i = tid; i < NL * MM; i += 128) Ms[i] = __ldg(mom + static_cast<size_t>(es) * NL * MM + i);
@@ -205,6 +206,28 @@ __global__ void __launch_bounds__(128) k_leaf_blocks(int ne, const int* __restri
       for (int nu = 0; nu < MM; ++nu) a = fma(Mt[la * MM + nu], T[nu * NL + lb], a);
       out[row_tile_off(cnt * NL, NL, la, kk * NL + lb)] = a;
     }
+  }
+}
+
+// near blocks (e, f), f >= e, copied into the block rows of the warp-specialised
+// leaf kernel (position k of row e; the diagonal block halved: the row's own
+// product and its transposed product each give half of it); one warp per block
+template <int NL>
+__global__ void __launch_bounds__(128) k_pack_sym_near(int n_pos, const int* __restrict__ slot_q,
+                                                       const int* __restrict__ eb, const int* __restrict__ rs,
+                                                       const int* __restrict__ near_a, const int* __restrict__ near_rs,
+                                                       const double* __restrict__ near, double* __restrict__ blk) {
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (k >= n_pos) return;
+  const int q = slot_q[k];
+  if (q < 0) return;
+  const int e = near_a[q];
+  const double scale = eb[k] == e ? 0.5 : 1.0;
+  const int r0 = rs[e], len = (rs[e + 1] - r0) * NL;
+  double* out = blk + static_cast<size_t>(r0) * NL * NL;
+  for (int i = lane; i < NL * NL; i += 32) {
+    const int la = i / NL, lb = i - la * NL;
+    out[row_tile_off(len, NL, la, (k - r0) * NL + lb)] = scale * near[near_off(near_a, near_rs, q, la, lb, NL)];
   }
 }
 

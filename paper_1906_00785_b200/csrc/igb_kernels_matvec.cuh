@@ -837,6 +837,24 @@ __global__ void k_far_lower(int n_nodes, int mm, const int* __restrict__ far_rs,
   down[idx] = acc;
 }
 
+// the same over an explicit list of slots per row (leaf blocks: only the pairs
+// the far kernels evaluate have a slot to add), ascending
+__global__ void k_far_lower_list(int n_nodes, int mm, const int* __restrict__ low_rs, const int* __restrict__ low_q,
+                                 const double* __restrict__ slot, double* __restrict__ down, int rows, int npp,
+                                 int leaf_off) {
+  pdl_entry();
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(n_nodes) * mm) return;
+  const int s = static_cast<int>(idx / mm), nu = static_cast<int>(idx % mm);
+  if (rows != 0 && ((s % npp >= leaf_off) != (rows == 1))) return;
+  const int k0 = low_rs[s], k1 = low_rs[s + 1];
+  if (k0 == k1) return;
+  double acc = down[idx];
+#pragma unroll 4
+  for (int k = k0; k < k1; ++k) acc += __ldcs(slot + static_cast<size_t>(__ldg(low_q + k)) * mm + nu);
+  down[idx] = acc;
+}
+
 // child(i,j) += tu^T X tv  (h2.cpp:328-347): children at level+1 >= 1 in
 // level-1 clusters [c0, c1); M as in k_up_level
 template <class S, int M>
@@ -1045,9 +1063,10 @@ __global__ void __launch_bounds__(256, MINB) k_far_col_near(
 // x NL test functions, contiguous: one copy) plus the coefficient vectors of
 // its blocks' source elements (one copy each).
 namespace ws {
-// 12 + 4 warps, 3 stages of one 17 KB tile each per stream warp (c5: leaf kernel
-// 5.84 ms; 13 + 3 warps 6.41, 14 + 2 warps 8.33)
-constexpr int kStreamWarps = 4, kFarWarps = 16 - kStreamWarps, kStages = 3;
+// 12 + 4 warps, 2 stages of one 17 KB tile each per stream warp (c5, kernel ms:
+// 6.33; 3 stages 6.42; 11 + 5 warps 6.54, 10 + 6 warps 7.09; with the leaf far
+// field still evaluated by half: 13 + 3 warps 6.41, 14 + 2 warps 8.33 against 5.84)
+constexpr int kStreamWarps = 4, kFarWarps = 16 - kStreamWarps, kStages = 2;
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -1140,8 +1159,8 @@ __global__ void __launch_bounds__(32 * (ws::kFarWarps + ws::kStreamWarps), 1) k_
   int n_rs = 0, n_re = 0, n_rs1 = 0, n_re1 = 0;
   auto fetch_item = [&](int e) {
     if (e < ne) {
-      n_rs = near_rs[e];
-      n_re = near_rs[e + 1];
+      n_rs = near_rs ? near_rs[e] : 0;  // null: the near field is part of the block rows
+      n_re = near_rs ? near_rs[e + 1] : 0;
       n_rs1 = lb.rs ? lb.rs[e] : 0;
       n_re1 = lb.rs ? lb.rs[e + 1] : 0;
     }
@@ -1151,7 +1170,7 @@ __global__ void __launch_bounds__(32 * (ws::kFarWarps + ws::kStreamWarps), 1) k_
     g_len = (n_re - n_rs) * NL;
     g_rs1 = n_rs1;
     g_len1 = (n_re1 - n_rs1) * NL;
-    g_seg = 0;
+    g_seg = g_len > 0 ? 0 : 1;
     g_j0 = 0;
     fetch_item(g_e + stride);
   };
@@ -1181,7 +1200,7 @@ __global__ void __launch_bounds__(32 * (ws::kFarWarps + ws::kStreamWarps), 1) k_
     const int rs = g_seg ? g_rs1 : g_rs, len = g_seg ? g_len1 : g_len;
     const int w = min(W, len - g_j0);
     const bool last_seg = g_seg == 1 || g_len1 == 0;
-    const bool first = g_seg == 0 && g_j0 == 0, last = last_seg && g_j0 + w >= len;
+    const bool first = g_j0 == 0 && (g_seg == 0 || g_len == 0), last = last_seg && g_j0 + w >= len;
     double* st = ring + s * LY::STAGE;
 #pragma unroll
     for (int h = 0; h < H; ++h) {

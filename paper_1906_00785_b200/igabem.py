@@ -634,10 +634,11 @@ class H2Matrix:
         return dict(leaf=int(out[0]), coarse=int(out[1]))
 
     def leaf_blocks(self):
-        """leaf-level far pairs applied as stored element blocks: (unordered pairs, bytes)"""
-        out = np.zeros(2, dtype=np.int64)
+        """leaf-level far pairs applied as stored element blocks: (unordered pairs, bytes of
+        their blocks, bytes of block rows -- near field + leaf blocks -- one matvec streams)"""
+        out = np.zeros(3, dtype=np.int64)
         _check(lib().igb_h2_leaf_blocks(self._h, _p(out, ctypes.c_longlong)))
-        return int(out[0]), int(out[1])
+        return int(out[0]), int(out[1]), int(out[2])
 
     def bench_steps(self, steps, matvecs):
         """steps x (device assembly + matvecs matvecs): (total ms, assembly ms) from CUDA events."""

@@ -43,9 +43,11 @@ def test_leaf_blocks_parity(igb, po, env, case):
         for frac in ("0", "0.3", "0.5", "1"):
             env["IGB_H2_LEAF_WS"], env["IGB_H2_LEAF_BLOCKS"] = ws, frac
             h = igb.H2Matrix(d, igb.H2Options(m=m, eta=1.6))
-            pairs, nbytes = h.leaf_blocks()
+            pairs, nbytes, stream = h.leaf_blocks()
             nl = d.local_count()
             assert nbytes == pairs * nl * nl * 8
+            near = h.device_bytes()["near"]
+            assert near // 2 < stream - nbytes <= near  # the near field: whole, or once per unordered pair
             leaf = h.far_sym_counts()["leaf"]
             if frac == "0":
                 assert pairs == 0
