@@ -105,7 +105,11 @@ int igb_h2_create(const igb_discretization* d, const igb_h2_opts* opts, int devi
  * (same values, no coupling storage).  Neither: Laplace evaluates on the fly,
  * Helmholtz / Maxwell store when the couplings fit in half the free device
  * memory (igb_h2_create always chooses this way). */
-enum { IGB_H2_STORED_COUPLINGS = 2, IGB_H2_DEVICE_PARTITION = 4, IGB_H2_FUSED_COUPLINGS = 8 };
+/* Setup: igb_h2_create(_ex) builds the element / cluster boxes, the block
+ * partition and the pair classes on the device (IGB_H2_DEVICE_PARTITION forces
+ * it, IGB_H2_HOST_PARTITION or the environment variable of that name selects
+ * the host code; the plans are bit-identical). */
+enum { IGB_H2_STORED_COUPLINGS = 2, IGB_H2_DEVICE_PARTITION = 4, IGB_H2_FUSED_COUPLINGS = 8, IGB_H2_HOST_PARTITION = 16 };
 int igb_h2_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int device, int flags, igb_h2** out);
 /* ---- multi-GPU row-cluster partition ----
  * rank `rank` of `world` assembles and applies the block rows of its level-1
@@ -209,9 +213,11 @@ void igb_h2_destroy(igb_h2* h);
  * traversal and pair classification of H2Matrix (h2.cpp:49-97,175-252) ---- */
 typedef struct igb_plan igb_plan;
 int igb_plan_create(const igb_discretization* d, const igb_h2_opts* opts, igb_plan** out);
-/* flags & IGB_H2_DEVICE_PARTITION (also for igb_h2_create_ex): the traversal,
-   sort, row starts and transposes of the block partition run on CUDA device
-   `device` (the lists are bit-identical to the host's) */
+/* flags & IGB_H2_DEVICE_PARTITION: the element boxes (spaces.cpp:117-147), the
+   cluster boxes and diagonals, the traversal, sort, row starts and transposes of
+   the block partition and the classes / maps of the near pairs
+   (spaces.cpp:309-394) are computed on CUDA device `device` (
+   bit-identical to the host's) */
 int igb_plan_create_ex(const igb_discretization* d, const igb_h2_opts* opts, int flags, int device, igb_plan** out);
 int igb_plan_counts(const igb_plan* p, long long* n_near, long long* n_far, int* n_nodes);
 int igb_plan_near_pairs(const igb_plan* p, int* out);
@@ -219,6 +225,10 @@ int igb_plan_far_pairs(const igb_plan* p, int* out);
 /* counts[0] = ordered regular near pairs, counts[1..3] = unique singular
  * pairs (vertex, edge, coincident) */
 int igb_plan_class_counts(const igb_plan* p, long long counts[4]);
+/* cluster boxes (ClusterTree, h2.cpp:49-78; leaves = the element boxes of
+ * spaces.cpp:117-147): out[node][6] = min xyz, max xyz.  A plan created on a
+ * device computes them there (with the traversal and the pair classes). */
+int igb_plan_node_boxes(const igb_plan* p, double* out);
 /* row-cluster partition over `world` ranks: rank owns the contiguous range
  * [*c0, *c1) of level-1 clusters (cluster = 4*patch + sx + 2*sy), i.e. the
  * block rows of their leaf elements; reports owned elements and the near /

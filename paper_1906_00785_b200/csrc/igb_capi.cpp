@@ -548,6 +548,17 @@ int igb_plan_class_counts(const igb_plan* p, long long counts[4]) {
     for (int c = 1; c <= 3; ++c) counts[c] = static_cast<long long>(p->plan.sing[c].ea.size());
   });
 }
+int igb_plan_node_boxes(const igb_plan* p, double* out) {
+  return guard([&] {
+    need(p, "plan");
+    need(out, "out");
+    for (size_t i = 0; i < p->plan.node_box.size(); ++i)
+      for (int k = 0; k < 3; ++k) {
+        out[6 * i + k] = p->plan.node_box[i].mn[k];
+        out[6 * i + 3 + k] = p->plan.node_box[i].mx[k];
+      }
+  });
+}
 int igb_plan_partition(const igb_plan* p, int world, int rank, int* c0, int* c1, int* n_elements,
                        long long* n_near, long long* n_far) {
   return guard([&] {

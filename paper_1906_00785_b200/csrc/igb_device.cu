@@ -291,7 +291,13 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   lap("stage 1 launched");
   // ---- stage 2: block partition on the host, overlapping the device
   const auto t0 = std::chrono::steady_clock::now();
-  plan_ = build_plan(d, opt_.m, opt_.eta, opt_.far_order, opt_.sing_order, (flags_ & 4) ? device_ : -1);
+  // the setup (boxes, traversal, sort, classes) runs on the device unless the host
+  // is asked for (flag 16 / IGB_H2_HOST_PARTITION) or a patch degree exceeds the
+  // device kernels' bound; both give bit-identical plans
+  bool dev_setup = !(flags_ & 16) && getenv("IGB_H2_HOST_PARTITION") == nullptr;
+  for (int p = 0; p < d.geometry().patch_count() && !(flags_ & 4); ++p)
+    if (d.geometry().patch(p).kv_u.degree > 15 || d.geometry().patch(p).kv_v.degree > 15) dev_setup = false;
+  plan_ = build_plan(d, opt_.m, opt_.eta, opt_.far_order, opt_.sing_order, ((flags_ & 4) || dev_setup) ? device_ : -1);
   lp_ = build_local_plan(d, plan_, opt_.world, opt_.rank);
   times_.plan_host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   lap("plan");

@@ -926,6 +926,29 @@ PairInfo Discretization::classify_pair(int ea, int eb) const {
   return info;
 }
 
+void Discretization::flatten_topology(std::vector<int>& edge_rs, std::vector<int>& edges, std::vector<int>& corner_rs,
+                                      std::vector<int>& corners) const {
+  const int np = geom_->patch_count();
+  edge_rs.assign(np * np + 1, 0);
+  corner_rs.assign(np * np + 1, 0);
+  edges.clear();
+  corners.clear();
+  for (int a = 0; a < np; ++a)
+    for (int b = 0; b < np; ++b) {
+      for (const auto& ce : cross_edges_[a][b]) {
+        edges.push_back(ce.edge_a);
+        edges.push_back(ce.edge_b);
+        edges.push_back(ce.reversed ? 1 : 0);
+      }
+      for (const auto& cc : cross_corners_[a][b]) {
+        corners.push_back(cc.corner_a);
+        corners.push_back(cc.corner_b);
+      }
+      edge_rs[a * np + b + 1] = static_cast<int>(edges.size() / 3);
+      corner_rs[a * np + b + 1] = static_cast<int>(corners.size() / 2);
+    }
+}
+
 void Discretization::singular_items(const unsigned char* owned, SingList out[4]) const {
   const int ne = element_count(), n = 1 << level_, np = geometry().patch_count();
   // patches sharing an edge / a corner with each patch
@@ -1100,7 +1123,9 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
           P.node_level[id] = l;
           P.node_sx[id] = sx;
           P.node_sy[id] = sy;
-          if (l == L) {
+          if (partition_device >= 0) {
+            // boxes come from the device (device_partition)
+          } else if (l == L) {
             P.node_box[id] = d.element(d.element_index(p, sx, sy)).box;
           } else {
             Box b;
@@ -1115,12 +1140,12 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
   // dual traversal (h2.cpp:198-216).  Same-level recursion from every ordered
   // root pair; decided pairs of levels 0-1 are collected serially and the
   // undecided level-2 pairs are traversed in parallel (balanced work list).
-  std::vector<double> diag(nn);
-  for (int i = 0; i < nn; ++i) diag[i] = P.node_box[i].diag_norm();
+  std::vector<double> diag(partition_device >= 0 ? 0 : nn);
   if (partition_device >= 0) {
-    device_partition(P, d, diag, eta, partition_device);
+    device_partition(P, d, eta, partition_device);
     lap("device partition");
   } else {
+  for (int i = 0; i < nn; ++i) diag[i] = P.node_box[i].diag_norm();
   auto child = [&](int node, int k) {
     return static_cast<int>(P.node_id(P.node_patch[node], P.node_level[node] + 1, 2 * P.node_sx[node] + (k & 1),
                                       2 * P.node_sy[node] + (k >> 1)));
@@ -1251,10 +1276,15 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
   }  // host partition
   const long long nnear = static_cast<long long>(P.near_a.size());
   // classification + unique singular work lists
+  const bool dev_cls = partition_device >= 0 && static_cast<long long>(P.near_cls.size()) == nnear;
   P.near_cls.resize(nnear);
   std::vector<uint8_t> mapa(nnear), mapb(nnear);
+  if (dev_cls) {  // classified on the device
+    mapa = P.dev_map_a;
+    mapb = P.dev_map_b;
+  }
 #pragma omp parallel for schedule(static)
-  for (long long q = 0; q < nnear; ++q) {
+  for (long long q = 0; q < (dev_cls ? 0 : nnear); ++q) {
     const int ea = P.near_a[q], eb = P.near_b[q];
     const PairInfo info = d.classify_pair(std::min(ea, eb), std::max(ea, eb));
     P.near_cls[q] = static_cast<uint8_t>(info.cls);

@@ -151,7 +151,14 @@ class Discretization {
   int element_index(int p, int ix, int iy) const { return p * epp_ + ix + (1 << level_) * iy; }
   const std::vector<int>& l2g() const { return l2g_; }
   const std::vector<double>& lsign() const { return lsign_; }
-  PairInfo classify_pair(int ea, int eb) const;  // spaces.cpp:309-394
+  PairInfo classify_pair(int ea, int eb) const;
+  // patch-pair topology tables of classify_pair, flattened for the device
+  // classification (igb_plan_gpu.cu): CSR over (patch a, patch b) of shared
+  // edges {edge_a, edge_b, reversed} and shared corners {corner_a, corner_b},
+  // in classify_pair's iteration order
+  void flatten_topology(std::vector<int>& edge_rs, std::vector<int>& edges, std::vector<int>& corner_rs,
+                        std::vector<int>& corners) const;
+ // spaces.cpp:309-394
   // The singular items (classify_pair class >= 1, ea <= eb) enumerated from the
   // mesh topology alone -- no block tree: same-patch neighbours, elements along
   // shared patch edges and at shared patch corners.  Ascending (ea, eb): the
@@ -229,6 +236,8 @@ struct H2Plan {
   std::vector<int> far_trans;       // per pair (t, s): index of (s, t)
   // near pair classification
   std::vector<uint8_t> near_cls;
+  // device setup (partition_device >= 0): map bits of the near pairs as classified on the device
+  std::vector<uint8_t> dev_map_a, dev_map_b;
   // unique singular work items per class (ea <= eb): element ids, map bits,
   // and the two output slots (slot of (ea,eb) and of (eb,ea); equal for
   // coincident pairs)
@@ -252,7 +261,10 @@ H2Plan build_plan(const Discretization& d, int m, double eta, int far_order, int
                   int partition_device = -1);
 // fills near_a/b, near_row_start, far_a/b, far_row_start, far_upper_start,
 // far_trans of P (tree and node boxes already built); igb_plan_gpu.cu
-void device_partition(H2Plan& P, const Discretization& d, const std::vector<double>& diag, double eta, int device);
+// ... and, on the device as well, the element boxes (spaces.cpp:117-147), the tree boxes
+// (h2.cpp:49-78), their diagonals and the classification of the near pairs
+// (spaces.cpp:309-394): node_box, near_cls, dev_map_a/b
+void device_partition(H2Plan& P, const Discretization& d, double eta, int device);
 // Option checks of build_plan (h2.hpp:60 ctor) and the quadrature orders it
 // derives (far: degree + 2, singular: degree + 3 unless given).
 void check_h2_options(const Discretization& d, int m, double eta, int far_order, int sing_order, int* nfar,

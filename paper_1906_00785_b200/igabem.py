@@ -90,7 +90,7 @@ SYMBOLS = (
     "igb_h2_gmres", "igb_h2_cg", "igb_rhs_points", "igb_rhs_assemble", "igb_potential", "igb_dense_assemble",
     "igb_h2_reassemble", "igb_h2_upload_bytes", "igb_h2_profile_apply", "igb_h2_bench_steps",
     "igb_h2_class_counts", "igb_h2_launch_counts", "igb_plan_create", "igb_plan_create_ex", "igb_plan_counts", "igb_plan_near_pairs",
-    "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
+    "igb_plan_far_pairs", "igb_plan_class_counts", "igb_plan_node_boxes", "igb_plan_partition", "igb_plan_owned", "igb_plan_singular_items",
     "igb_plan_destroy", "igb_h2_destroy", "igb_admissible", "igb_last_error", "igb_version",
     "igb_release_device_memory", "igb_h2_profile_kernels", "igb_h2_far_work", "igb_h2_leaf_blocks", "igb_h2_far_field", "igb_h2_dist_dof_mask",
 )
@@ -158,6 +158,7 @@ def lib():
     L.igb_plan_near_pairs.argtypes = [vp, P(i32)]
     L.igb_plan_far_pairs.argtypes = [vp, P(i32)]
     L.igb_plan_class_counts.argtypes = [vp, P(i64)]
+    L.igb_plan_node_boxes.argtypes = [vp, P(f64)]
     L.igb_plan_partition.argtypes = [vp, i32, i32, P(i32), P(i32), P(i32), P(i64), P(i64)]
     L.igb_plan_owned.argtypes = [vp, i32, i32, P(ctypes.c_ubyte), P(ctypes.c_ubyte)]
     L.igb_plan_singular_items.argtypes = [vp, i32, i32, P(ctypes.c_longlong), P(i32)]
@@ -411,6 +412,12 @@ class H2Plan:
         _check(lib().igb_plan_class_counts(self._h, _p(out, ctypes.c_longlong)))
         return dict(regular=int(out[0]), vertex=int(out[1]), edge=int(out[2]), coincident=int(out[3]))
 
+    def node_boxes(self):
+        """cluster boxes [node][min xyz, max xyz] (leaves: the element boxes)"""
+        out = np.zeros((self.node_count, 6))
+        _check(lib().igb_plan_node_boxes(self._h, _p(out, ctypes.c_double)))
+        return out
+
     def partition(self, world, rank):
         c0, c1, ne = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         nn, nf = ctypes.c_longlong(), ctypes.c_longlong()
@@ -444,13 +451,14 @@ class H2Matrix:
 
     def __init__(self, disc: Discretization, opts: H2Options | None = None, device: int = 0,
                  stored_couplings: bool | None = None, world: int = 1, rank: int = 0,
-                 device_partition: bool = False):
+                 device_partition: Optional[bool] = None):
         opts = opts or H2Options()
         o = _Opts(int(opts.m), float(opts.eta), int(opts.quad.far_order), int(opts.quad.sing_order))
         h = ctypes.c_void_p()
         # stored_couplings: True -> stream stored couplings, False -> evaluate them
         # in every matvec, None -> chosen per kind and size (include/igabem_b200.h)
-        flags = {True: 2, False: 8, None: 0}[stored_couplings] | (4 if device_partition else 0)
+        # device_partition: None = the library's default (device), True / False force device / host
+        flags = {True: 2, False: 8, None: 0}[stored_couplings] | {True: 4, False: 16, None: 0}[device_partition]
         if world == 1:
             _check(lib().igb_h2_create_ex(disc._h, ctypes.byref(o), int(device), flags, ctypes.byref(h)))
         else:

@@ -8,7 +8,7 @@ sys.path.insert(0, ".")
 import paper_1906_00785_b200 as igb
 from bench import CONFIGS, make_disc
 c = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c5"]
-dp = len(sys.argv) > 2
+dp = {"dp": True, "host": False}.get(sys.argv[2]) if len(sys.argv) > 2 else None
 d = make_disc(igb, c)
 for it in range(3):
     t = time.perf_counter()
