@@ -1108,7 +1108,7 @@ __device__ __forceinline__ void cp_arrive(unsigned long long* bar) {
 template <int M, int NL>
 struct Layout {
   static constexpr int SLAB = (5 * M * M + 1) / 2 * 2;             // far warp: target rows + moments
-  static constexpr int STAGE = (NL + 1) * kRowTile;                // stream stage: tile [NL][w] + coefficients [w]
+  static constexpr int STAGE = (NL + 1) * kRowTile + NL;           // stream stage: tile [NL][w] + coefficients [w] + the row element's own [NL]
   static constexpr int FAR0 = 0;
   static constexpr int RING0 = (kFarWarps * SLAB + 15) / 16 * 16;  // doubles, 128 B aligned
   static constexpr int XT0 = RING0 + kStreamWarps * kStages * STAGE;
@@ -1207,6 +1207,9 @@ __global__ void __launch_bounds__(32 * (ws::kFarWarps + ws::kStreamWarps), 1) k_
       const int c = 2 * lane + 64 * h;
       if (c < w) ws::cp16_g2s(st + NL * W + c, coef + static_cast<size_t>(pf_e[h]) * NL + (g_j0 + c) % NL);
     }
+    // first slice of a row's blocks: the row element's own coefficients ride along
+    if (g_seg == 1 && g_j0 == 0 && 2 * lane < NL)
+      ws::cp16_g2s(st + (NL + 1) * W + 2 * lane, coef + static_cast<size_t>(g_e) * NL + 2 * lane);
     ws::cp_arrive(bar + s);
     if (lane == 0) {
       desc[s] = make_int4(g_e, rs * NL + g_j0, w, (first ? 1 : 0) | (last ? 2 : 0) | (g_seg ? 4 : 0) | ((g_seg && g_j0 == 0) ? 8 : 0));
@@ -1237,8 +1240,8 @@ __global__ void __launch_bounds__(32 * (ws::kFarWarps + ws::kStreamWarps), 1) k_
     ws::mbar_wait(bar + s, (consumed / NS) & 1);
     const int4 d = desc[s];
     const double* st = ring + s * LY::STAGE;
-    if (d.w & 8) {  // first slice of the leaf blocks: this element's coefficients
-      if (lane < NL) xt[lane] = coef[static_cast<size_t>(d.x) * NL + lane];
+    if (d.w & 8) {  // first slice of the row's blocks: this element's coefficients
+      if (lane < NL) xt[lane] = st[(NL + 1) * W + lane];
       __syncwarp();
     }
     if (d.w & 1) {
