@@ -1179,9 +1179,20 @@ void H2Device::enqueue_apply_split(const double* xin, double* yout, cudaStream_t
   }
   if (!prof) IGB_CUDA(cudaEventRecord(ev_join_, side_));
   const long long ndown = static_cast<long long>(P.n_nodes) * rows;
-  pdl_launch(k_leaf_up_x<S, NL>, grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s, 
-      nel, rows, epp, npp, P.level_offset[L], d_mom_, x, d_l2g_, d_lsign_, up, down, ndown,
-      static_cast<S*>(leaf_ws ? coef : nullptr));
+  bool up_w = false;
+  if constexpr (KT::KIND == 0 && NL == 16) {
+    if (leaf_ws && nel == d.element_count() && rows <= 32) {  // one warp per element, coalesced moments
+      up_w = true;
+      pdl_launch(k_leaf_up_w<NL>, grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s, nel, rows, epp, npp,
+          P.level_offset[L], static_cast<const double*>(d_mom_), reinterpret_cast<const double*>(x),
+          static_cast<const int*>(d_l2g_), static_cast<const double*>(d_lsign_), reinterpret_cast<double*>(up),
+          reinterpret_cast<double*>(down), ndown, reinterpret_cast<double*>(coef));
+    }
+  }
+  if (!up_w)
+    pdl_launch(k_leaf_up_x<S, NL>, grid_for(std::max(ndown, static_cast<long long>(nel) * rows), 256), 256, 0, s,
+        nel, rows, epp, npp, P.level_offset[L], d_mom_, x, d_l2g_, d_lsign_, up, down, ndown,
+        static_cast<S*>(leaf_ws ? coef : nullptr));
   ++launches;
   tick("leaf_up");
   if (!prof && !leaf_ws) {

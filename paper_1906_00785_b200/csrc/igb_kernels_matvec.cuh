@@ -63,6 +63,44 @@ __global__ void k_leaf_up_x(int n_el, int rows, int epp, int npp, int leaf_off, 
   up[static_cast<size_t>(leaf) * rows + r] = acc;
 }
 
+// The same with one warp per element (real scalars; the warp-specialised graph):
+// the element's moments [l][row] are staged in shared memory by coalesced loads
+// and lane r sums its row in the same FMA order, so the results are bit-identical
+// to k_leaf_up_x; also writes the element coefficients and zeroes down.
+template <int NL>
+__global__ void __launch_bounds__(256) k_leaf_up_w(int n_el, int rows, int epp, int npp, int leaf_off,
+                                                   const double* __restrict__ mom, const double* __restrict__ x,
+                                                   const int* __restrict__ l2g, const double* __restrict__ sg,
+                                                   double* __restrict__ up, double* __restrict__ down, long long ndown,
+                                                   double* __restrict__ coef_out) {
+  pdl_entry();
+  constexpr int MAXR = 32;  // rows <= 32 (m <= 5)
+  __shared__ double sh[8][NL * MAXR + NL];
+  const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long total = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = tid; i < ndown; i += total) down[i] = 0.0;
+  const int e = static_cast<int>(tid >> 5), lane = threadIdx.x & 31;
+  if (e >= n_el) return;
+  double* ms = sh[threadIdx.x >> 5];
+  double* cs = ms + NL * MAXR;
+  const double* me = mom + static_cast<size_t>(e) * NL * rows;
+  for (int i = lane; i < NL * rows; i += 32) ms[i] = __ldg(me + i);
+  if (lane < NL) {
+    const int k = e * NL + lane;
+    const double c = x[l2g[k]] * sg[k];
+    cs[lane] = c;
+    coef_out[k] = c;
+  }
+  __syncwarp();
+  if (lane < rows) {
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc = fma(cs[l], ms[l * rows + lane], acc);
+    const int leaf = (e / epp) * npp + leaf_off + (e % epp);
+    up[static_cast<size_t>(leaf) * rows + lane] = acc;
+  }
+}
+
 // node of a level-l tree in level-1 cluster c (l >= 1), local index sc
 __device__ __forceinline__ void cluster_node(int c, int level, int sc, int& p, int& sx, int& sy) {
   const int half = 1 << (level - 1);
