@@ -654,6 +654,36 @@ void H2Device::stage_plan() {
           lb_lap("uploads");
         }
       }
+      // Helmholtz: all leaf-level far pairs as complex element blocks (ordered rows)
+      if (sym_w_ && d.kind() == kHelmholtz && ident && P.depth >= 1) {
+        double frac = 1.0;
+        if (const char* env = getenv("IGB_H2_LEAF_BLOCKS")) frac = atof(env);
+        const int ne = d.element_count(), epp = d.elements_per_patch(), leaf_off = P.level_offset[P.depth];
+        std::vector<int> cb_rs(ne + 1, 0);
+        for (int e = 0; e < ne; ++e) {
+          const int t = (e / epp) * P.npp + leaf_off + e % epp;
+          cb_rs[e + 1] = cb_rs[e] + (P.far_row_start[t + 1] - P.far_row_start[t]);
+        }
+        const double need = static_cast<double>(cb_rs[ne]) * NL * NL * 16.0;
+        if (frac > 0.0 && cb_rs[ne] > 0 && need <= 0.25 * static_cast<double>(available_device_bytes(device_))) {
+          std::vector<int> eb(cb_rs[ne]);
+#pragma omp parallel for schedule(static)
+          for (int e = 0; e < ne; ++e) {
+            const int t = (e / epp) * P.npp + leaf_off + e % epp;
+            for (int q = P.far_row_start[t], k = cb_rs[e]; q < P.far_row_start[t + 1]; ++q, ++k) {
+              const int sq = P.far_b[q];
+              eb[k] = (sq / P.npp) * epp + (sq % P.npp - leaf_off);
+            }
+          }
+          d_cb_rs_ = upload(cb_rs);
+          d_cb_eb_ = upload(eb);
+          d_cb_blk_ = dalloc<double>(static_cast<size_t>(cb_rs[ne]) * NL * NL * 2);
+          cblk_ = true;
+          n_leaf_blocks_ = cb_rs[ne] / 2;
+          leaf_block_bytes_ = static_cast<size_t>(cb_rs[ne]) * NL * NL * 16;
+          sym_pairs_[0] = 0;
+        }
+      }
       if (Lp.world > 1 && sym_far_ && m <= 5) {  // per-target column lists for k_far_col_list
         std::vector<int> col_rs(1, 0), col_q;
         for (int t : sym_targets) {
@@ -788,6 +818,17 @@ void H2Device::launch_plan_phase(cudaEvent_t* ev, int& launched) {
       IGB_CUDA(cudaGetLastError());
     }
   }
+  if (cblk_) {
+    if constexpr (KT::KIND == 1) {
+      const size_t smem = (static_cast<size_t>(2 * NL * mm + 6 * mm + 1) + 2 * (static_cast<size_t>(mm) * mm + mm * NL)) * 8;
+      IGB_CUDA(cudaFuncSetAttribute(k_leaf_blocks_c<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      k_leaf_blocks_c<KT><<<d.element_count(), 128, smem, stream_>>>(
+          d.element_count(), m, d_cb_rs_, d_far_rs_, d_far_b_, d_upper_start_, d_trans_, d.elements_per_patch(), P.npp,
+          P.level_offset[P.depth], d_img_, d_mom_, g.kp, reinterpret_cast<S*>(d_cb_blk_));
+      ++launched;
+      IGB_CUDA(cudaGetLastError());
+    }
+  }
   IGB_CUDA(cudaEventRecord(ev[kEvImages], stream_));
   if (nfarp > 0 && stored_couplings()) {  // fused mode evaluates the couplings inside the matvec
     k_couplings<KT><<<148 * 16, 256, 0, stream_>>>(nfarp, mm, d_far_a_, d_far_b_, d_img_, g.kp, d_far_);
@@ -905,6 +946,11 @@ void H2Device::enqueue_phase1(const double* xin, double* send, cudaStream_t s, c
     k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
         nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
     ++launches;
+    if (cblk_ && !far_only_) {  // + the leaf blocks of the complex kinds
+      k_block_rows_acc<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, side_>>>(
+          nel, d_cb_rs_, d_cb_eb_, reinterpret_cast<const S*>(d_cb_blk_), coef, nrows);
+      ++launches;
+    }
     IGB_CUDA(cudaEventRecord(ev_join_, side_));
   }
   pdl_launch(k_leaf_up<S, NL>, grid_for(static_cast<long long>(nel) * rows, 256), 256, 0, s, 
@@ -1048,26 +1094,31 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
       kp.dwx = as_.kp[2];
       kp.dwy = as_.kp[3];
       constexpr int PW = ((4 + KT::NC * static_cast<int>(sizeof(S) / 8)) + 1) / 2 * 2;
-      const unsigned gsym = grid_for(static_cast<long long>(n_sym_targets_) * 32, 256);
+      // leaf blocks (Helmholtz): the leaf level is applied as blocks, the far kernel keeps the rest
+      const bool cb = cblk_ && !far_only_;
+      const int n_tg = cb ? n_sym_coarse_ : n_sym_targets_;
+      const int* tg = cb ? d_sym_coarse_ : d_sym_targets_;
+      const unsigned gsym = grid_for(static_cast<long long>(std::max(n_tg, 1)) * 32, 256);
       S* sl = reinterpret_cast<S*>(d_slot_);
       const int R = (mm + 31) / 32;
       const size_t smem = static_cast<size_t>(8) * 32 * R * PW * 8;
       if (R == 1)
-        k_far_sym_w<KT, 1><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+        k_far_sym_w<KT, 1><<<gsym, 256, smem, s>>>(n_tg, tg, d_upper_start_, d_far_rs_, d_far_b_,
                                                    d_trans_, d_img_, mm, up, kp, down, sl);
       else if (R == 2)
-        k_far_sym_w<KT, 2><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+        k_far_sym_w<KT, 2><<<gsym, 256, smem, s>>>(n_tg, tg, d_upper_start_, d_far_rs_, d_far_b_,
                                                    d_trans_, d_img_, mm, up, kp, down, sl);
       else if (R == 3)
-        k_far_sym_w<KT, 3><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+        k_far_sym_w<KT, 3><<<gsym, 256, smem, s>>>(n_tg, tg, d_upper_start_, d_far_rs_, d_far_b_,
                                                    d_trans_, d_img_, mm, up, kp, down, sl);
       else
-        k_far_sym_w<KT, 4><<<gsym, 256, smem, s>>>(n_sym_targets_, d_sym_targets_, d_upper_start_, d_far_rs_, d_far_b_,
+        k_far_sym_w<KT, 4><<<gsym, 256, smem, s>>>(n_tg, tg, d_upper_start_, d_far_rs_, d_far_b_,
                                                    d_trans_, d_img_, mm, up, kp, down, sl);
       ++launches;
       const int stride = rows * static_cast<int>(sizeof(S) / 8);
       pdl_launch(k_far_lower<false>, grid_for(static_cast<long long>(P.n_nodes) * stride, 256), 256, 0, s, 
-          P.n_nodes, stride, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, reinterpret_cast<double*>(down), 0, 1, 0);
+          P.n_nodes, stride, d_far_rs_, d_upper_start_, d_far_b_, d_owned_, d_slot_, reinterpret_cast<double*>(down),
+          cb ? 2 : 0, cb ? npp : 1, cb ? P.level_offset[L] : 0);
     } else {
       KParams kp;
       kp.kr = as_.kp[0];
@@ -1097,6 +1148,11 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
     k_near_rows<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s>>>(
         nel, d_near_rs_, d_near_b_, reinterpret_cast<const S*>(d_near_), coef, nrows);
     ++launches;
+    if (cblk_) {
+      k_block_rows_acc<S, NL><<<grid_for(static_cast<long long>(nel) * 32, 256), 256, 0, s>>>(
+          nel, d_cb_rs_, d_cb_eb_, reinterpret_cast<const S*>(d_cb_blk_), coef, nrows);
+      ++launches;
+    }
   }
   mark(6);
   for (int l = 0; l < L; ++l) {

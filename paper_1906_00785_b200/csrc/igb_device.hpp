@@ -177,6 +177,11 @@ class H2Device {
   int n_lb_total_ = 0;        // block-row positions: blocked far pairs (+ near pairs f >= e when lb_sym_near_)
   bool lb_sym_near_ = false;  // k_leaf_ws: the near field is part of the block rows (stored once per unordered pair)
   int* d_lb_nq_ = nullptr;
+  // Helmholtz (one GPU): every leaf-level far pair as a complex element block in rows added
+  // to the near rows (k_leaf_blocks_c / k_block_rows_acc); the far kernel keeps the coarse levels
+  bool cblk_ = false;
+  int *d_cb_rs_ = nullptr, *d_cb_eb_ = nullptr;
+  double* d_cb_blk_ = nullptr;
   int *d_low_rs_ = nullptr, *d_low_q_ = nullptr;  // per node: the lower pairs whose slots are written
   int *d_upper_end_ = nullptr, *d_lb_rs_ = nullptr, *d_lb_eb_ = nullptr, *d_lb_ns_ = nullptr;
   int *d_lb_in_rs_ = nullptr, *d_lb_in_k_ = nullptr;

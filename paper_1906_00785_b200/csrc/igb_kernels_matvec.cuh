@@ -1014,7 +1014,8 @@ __device__ __forceinline__ void near_row_seg(S (&acc)[NL], int e, int lane, cons
     if constexpr (SYM) tslot[static_cast<size_t>(rs) * NL + j] = ps;
   }
 }
-template <class S, int NL, bool FROM_X>
+// ACC: add to rows_out (a second set of block rows of the same elements)
+template <class S, int NL, bool FROM_X, bool ACC = false>
 __device__ __forceinline__ void near_row(int e, int lane, const int* __restrict__ near_rs,
                                          const int* __restrict__ near_b, const S* __restrict__ blk,
                                          const S* __restrict__ coef, S* __restrict__ rows_out,
@@ -1026,8 +1027,21 @@ __device__ __forceinline__ void near_row(int e, int lane, const int* __restrict_
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
     const S a = warp_sum(acc[l]);
-    if (lane == 0) rows_out[static_cast<size_t>(e) * NL + l] = a;
+    if (lane == 0) {
+      if constexpr (ACC) rows_out[static_cast<size_t>(e) * NL + l] = rows_out[static_cast<size_t>(e) * NL + l] + a;
+      else rows_out[static_cast<size_t>(e) * NL + l] = a;
+    }
   }
+}
+// the leaf blocks of the complex kinds (k_leaf_blocks_c): added to the near rows
+template <class S, int NL>
+__global__ void __launch_bounds__(256) k_block_rows_acc(int ne, const int* __restrict__ rs, const int* __restrict__ eb,
+                                                        const S* __restrict__ blk, const S* __restrict__ coef,
+                                                        S* __restrict__ rows_out) {
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (e >= ne) return;
+  if (rs[e] == rs[e + 1]) return;
+  near_row<S, NL, false, true>(e, threadIdx.x & 31, rs, eb, blk, coef, rows_out, nullptr, nullptr);
 }
 template <class S, int NL, bool FROM_X = false>
 __global__ void __launch_bounds__(256) k_near_rows(int ne, const int* __restrict__ near_rs,

@@ -79,3 +79,31 @@ def test_leaf_blocks_far_field_matches_unblocked(igb, env):
     env["IGB_H2_LEAF_BLOCKS"] = "0.5"
     _, down1 = igb.H2Matrix(d, igb.H2Options(m=5)).far_field(x)
     assert np.array_equal(down0, down1)
+
+
+def test_helmholtz_leaf_blocks(igb, po, env):
+    """Helmholtz: every leaf-level far pair as a complex element block
+    (k_leaf_blocks_c, rows added to the near rows) against the oracle, with
+    the blocks on (default) and off (all couplings evaluated)."""
+    kappa = 3.0 + 0j
+    od = po.Discretization("helmholtz", 3, 1, 3, kappa=kappa)
+    oh = po.H2Matrix(od, m=8, eta=1.6)
+    rng = np.random.default_rng(20261019)
+    x = rng.uniform(-1, 1, od.dof_count) + 1j * rng.uniform(-1, 1, od.dof_count)
+    yr = oh.apply(x)
+    d = igb.Discretization(igb.make_sphere(), igb.Pde.helmholtz(kappa), 3, 1, 3)
+    got = {}
+    for frac in ("1", "0"):
+        env["IGB_H2_LEAF_BLOCKS"] = frac
+        h = igb.H2Matrix(d, igb.H2Options(m=8, eta=1.6))
+        pairs, nbytes, _ = h.leaf_blocks()
+        assert (pairs > 0) == (frac == "1")
+        y = h.apply(x)
+        rel = np.linalg.norm(y - yr) / np.linalg.norm(yr)
+        assert rel < TOL, f"blocks={frac}: {rel:.3e}"
+        assert np.array_equal(h.apply(x), y)
+        up, down = h.far_field(x)  # introspection: all pairs evaluated
+        got[frac] = down
+        h.reassemble()
+        assert np.array_equal(h.apply(x), y)
+    assert np.array_equal(got["1"], got["0"])
