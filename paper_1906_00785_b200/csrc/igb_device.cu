@@ -306,10 +306,15 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   // complex kernel evaluations per pair cost more than streaming the block
   // (c4: 6.2 ms per matvec stored at 93 % of HBM vs 14.6 ms evaluated); Laplace
   // always evaluates them (c5: the symmetric FP64 kernel beats the 161 GB stream)
+  // -- unless the leaf level can be applied as element blocks (k_leaf_blocks_c: the
+  // warp-row symmetric kernel then evaluates only the coarse levels; c4: 5.1 ms
+  // against 6.0 ms streaming the stored couplings, c3: 22 ms against 80 ms)
   if (!(flags_ & (kStoredCouplings | kFusedCouplings)) && opt_.world == 1 && d.is_complex()) {
     const size_t free_b = available_device_bytes(device_);
     const size_t mm = static_cast<size_t>(opt_.m) * opt_.m;
-    if (plan_.far_a.size() * mm * mm * 16 <= free_b / 2) flags_ |= kStoredCouplings;
+    const char* lbe = getenv("IGB_H2_LEAF_BLOCKS");
+    const bool blocks_ok = (lbe == nullptr || atof(lbe) > 0.0) && mm >= 32 && mm <= 128 && plan_.depth >= 2;
+    if (!blocks_ok && plan_.far_a.size() * mm * mm * 16 <= free_b / 2) flags_ |= kStoredCouplings;
   }
   for (int c = 1; c <= 3; ++c) {  // topology items == the near list's singular pairs
     const SingList &T = sing_items_[c], &L = lp_.sing[c];
@@ -655,7 +660,7 @@ void H2Device::stage_plan() {
         }
       }
       // Helmholtz: all leaf-level far pairs as complex element blocks (ordered rows)
-      if (sym_w_ && d.kind() == kHelmholtz && ident && P.depth >= 1) {
+      if (sym_w_ && d.is_complex() && ident && P.depth >= 1) {
         double frac = 1.0;
         if (const char* env = getenv("IGB_H2_LEAF_BLOCKS")) frac = atof(env);
         const int ne = d.element_count(), epp = d.elements_per_patch(), leaf_off = P.level_offset[P.depth];
@@ -819,8 +824,8 @@ void H2Device::launch_plan_phase(cudaEvent_t* ev, int& launched) {
     }
   }
   if (cblk_) {
-    if constexpr (KT::KIND == 1) {
-      const size_t smem = (static_cast<size_t>(2 * NL * mm + 6 * mm + 1) + 2 * (static_cast<size_t>(mm) * mm + mm * NL)) * 8;
+    if constexpr (KT::KIND != 0) {
+      const size_t smem = (static_cast<size_t>(2 * NL * nch_ * mm + 6 * mm + 1) + 2 * (static_cast<size_t>(mm) * mm + static_cast<size_t>(nch_) * mm * NL)) * 8;
       IGB_CUDA(cudaFuncSetAttribute(k_leaf_blocks_c<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       k_leaf_blocks_c<KT><<<d.element_count(), 128, smem, stream_>>>(
           d.element_count(), m, d_cb_rs_, d_far_rs_, d_far_b_, d_upper_start_, d_trans_, d.elements_per_patch(), P.npp,

@@ -209,12 +209,15 @@ __global__ void __launch_bounds__(128) k_leaf_blocks(int ne, const int* __restri
   }
 }
 
-// Complex kinds with one channel (Helmholtz): every leaf-level admissible pair as an
-// element block B = mom_t K mom_s^T (complex; the moments are real), so the
-// matvec streams nl^2 scalars per ordered pair instead of evaluating m^4 complex
-// kernels per unordered pair (c3: 81 against 4096).  One CTA per element t walks
-// the row's pairs with s > t and writes B into row t and B^T into row s (the
-// kernel is symmetric); rows are the ordered far rows of the leaf nodes.
+// Complex kinds: every leaf-level admissible pair as an element block
+//   B = sum_c w_c mom_t,c K mom_s,c^T   (complex; the moments are real; channels
+// c of the Maxwell EFIE share the scalar kernel K, the divergence channel carries
+// the weight -1/kappa^2), so the matvec streams nl^2 scalars per ordered pair
+// instead of evaluating m^4 complex kernels per unordered pair (c3: 81 against
+// 4096) or streaming the stored coupling (c4: 2.3 KB against 65 KB).  One CTA
+// per element t walks the row's pairs with s > t and writes B into row t and
+// B^T into row s (the kernel is symmetric); rows are the ordered far rows of
+// the leaf nodes.
 template <class KT>
 __global__ void __launch_bounds__(128) k_leaf_blocks_c(int ne, int m, const int* __restrict__ rs,
                                                        const int* __restrict__ far_rs, const int* __restrict__ far_b,
@@ -223,28 +226,29 @@ __global__ void __launch_bounds__(128) k_leaf_blocks_c(int ne, int m, const int*
                                                        const double* __restrict__ mom, KParams kp,
                                                        typename KT::S* __restrict__ blk) {
   using S = typename KT::S;
-  constexpr int NL = KT::NL;
-  const int mm = m * m;
+  constexpr int NL = KT::NL, NCH = KT::NC;
+  const int mm = m * m, rows = NCH * mm;
   extern __shared__ __align__(16) double cbsm[];
   double* Mt = cbsm;
-  double* Ms = Mt + NL * mm;
-  double* it = Ms + NL * mm;
+  double* Ms = Mt + NL * rows;
+  double* it = Ms + NL * rows;
   double* is = it + 3 * mm;
-  S* K = reinterpret_cast<S*>(is + 3 * mm + ((NL * mm * 2 + 6 * mm) & 1));
-  S* T = K + mm * mm;
+  S* K = reinterpret_cast<S*>(is + 3 * mm + ((NL * rows * 2 + 6 * mm) & 1));
+  S* T = K + mm * mm;  // [c][nu][lb]
   const int e = blockIdx.x, tid = threadIdx.x;
   if (e >= ne) return;
   const int t = (e / epp) * npp + leaf_off + e % epp;
   const int q_lo = upper_start[t], q_hi = far_rs[t + 1];
   if (q_lo == q_hi) return;
   const int r0 = rs[e], cnt = rs[e + 1] - r0;
-  for (int i = tid; i < NL * mm; i += 128) Mt[i] = __ldg(mom + static_cast<size_t>(e) * NL * mm + i);
+  const S wdiv = mk(kp.dwx, kp.dwy);
+  for (int i = tid; i < NL * rows; i += 128) Mt[i] = __ldg(mom + static_cast<size_t>(e) * NL * rows + i);
   for (int i = tid; i < 3 * mm; i += 128) it[i] = __ldg(img + static_cast<size_t>(t) * 3 * mm + i);
   for (int q = q_lo; q < q_hi; ++q) {
     const int s = far_b[q];
     const int es = (s / npp) * epp + (s % npp - leaf_off);
     __syncthreads();
-    for (int i = tid; i < NL * mm; i += 128) Ms[i] = __ldg(mom + static_cast<size_t>(es) * NL * mm + i);
+    for (int i = tid; i < NL * rows; i += 128) Ms[i] = __ldg(mom + static_cast<size_t>(es) * NL * rows + i);
     for (int i = tid; i < 3 * mm; i += 128) is[i] = __ldg(img + static_cast<size_t>(s) * 3 * mm + i);
     __syncthreads();
     for (int i = tid; i < mm * mm; i += 128) {
@@ -253,19 +257,21 @@ __global__ void __launch_bounds__(128) k_leaf_blocks_c(int ne, int m, const int*
       K[i] = green_k<KT>(d0 * d0 + d1 * d1 + d2 * d2, kp);
     }
     __syncthreads();
-    for (int i = tid; i < mm * NL; i += 128) {  // T[nu][lb] = sum_mu K[nu][mu] Ms[lb][mu]
-      const int nu = i / NL, lb = i - nu * NL;
+    for (int i = tid; i < NCH * mm * NL; i += 128) {  // T_c[nu][lb] = sum_mu K[nu][mu] Ms[lb][c mm + mu]
+      const int c = i / (mm * NL), r = i - c * mm * NL, nu = r / NL, lb = r - nu * NL;
       S a = zero<S>();
-      for (int mu = 0; mu < mm; ++mu) fmac(a, K[nu * mm + mu], Ms[lb * mm + mu]);
+      for (int mu = 0; mu < mm; ++mu) fmac(a, K[nu * mm + mu], Ms[lb * rows + c * mm + mu]);
+      if (NCH == 4 && c == 3) a = a * wdiv;
       T[i] = a;
     }
     __syncthreads();
     const int kk = q - far_rs[t];
     const int qt = trans[q], rs_s = rs[es], cnt_s = rs[es + 1] - rs_s, kk_s = qt - far_rs[s];
-    for (int i = tid; i < NL * NL; i += 128) {  // B[la][lb] = sum_nu Mt[la][nu] T[nu][lb]
+    for (int i = tid; i < NL * NL; i += 128) {  // B[la][lb] = sum_c sum_nu Mt[la][c mm + nu] T_c[nu][lb]
       const int la = i / NL, lb = i - la * NL;
       S a = zero<S>();
-      for (int nu = 0; nu < mm; ++nu) fmac(a, T[nu * NL + lb], Mt[la * mm + nu]);
+      for (int c = 0; c < NCH; ++c)
+        for (int nu = 0; nu < mm; ++nu) fmac(a, T[(c * mm + nu) * NL + lb], Mt[la * rows + c * mm + nu]);
       blk[static_cast<size_t>(r0) * NL * NL + row_tile_off(cnt * NL, NL, la, kk * NL + lb)] = a;
       blk[static_cast<size_t>(rs_s) * NL * NL + row_tile_off(cnt_s * NL, NL, lb, kk_s * NL + la)] = a;
     }
