@@ -306,15 +306,12 @@ void H2Device::assemble_impl(std::chrono::steady_clock::time_point t_wall0) {
   // complex kernel evaluations per pair cost more than streaming the block
   // (c4: 6.2 ms per matvec stored at 93 % of HBM vs 14.6 ms evaluated); Laplace
   // always evaluates them (c5: the symmetric FP64 kernel beats the 161 GB stream)
-  // -- unless the leaf level can be applied as element blocks (k_leaf_blocks_c: the
-  // warp-row symmetric kernel then evaluates only the coarse levels; c4: 5.1 ms
-  // against 6.0 ms streaming the stored couplings, c3: 22 ms against 80 ms)
+  // (either way the leaf level of the complex kinds is applied as element blocks,
+  // k_leaf_blocks_c, and only the coarse levels stream / evaluate couplings)
   if (!(flags_ & (kStoredCouplings | kFusedCouplings)) && opt_.world == 1 && d.is_complex()) {
     const size_t free_b = available_device_bytes(device_);
     const size_t mm = static_cast<size_t>(opt_.m) * opt_.m;
-    const char* lbe = getenv("IGB_H2_LEAF_BLOCKS");
-    const bool blocks_ok = (lbe == nullptr || atof(lbe) > 0.0) && mm >= 32 && mm <= 128 && plan_.depth >= 2;
-    if (!blocks_ok && plan_.far_a.size() * mm * mm * 16 <= free_b / 2) flags_ |= kStoredCouplings;
+    if (plan_.far_a.size() * mm * mm * 16 <= free_b / 2) flags_ |= kStoredCouplings;
   }
   for (int c = 1; c <= 3; ++c) {  // topology items == the near list's singular pairs
     const SingList &T = sing_items_[c], &L = lp_.sing[c];
@@ -499,6 +496,38 @@ void H2Device::stage_plan() {
     const std::vector<int>& targets = Lp.far_targets;
     n_far_targets_ = static_cast<int>(targets.size());
     d_far_targets_ = upload(targets);
+    // complex kinds: all leaf-level far pairs as complex element blocks (ordered rows)
+    auto setup_cblk = [&]() {
+      {
+        double frac = 1.0;
+        if (const char* env = getenv("IGB_H2_LEAF_BLOCKS")) frac = atof(env);
+        const int ne = d.element_count(), epp = d.elements_per_patch(), leaf_off = P.level_offset[P.depth];
+        std::vector<int> cb_rs(ne + 1, 0);
+        for (int e = 0; e < ne; ++e) {
+          const int t = (e / epp) * P.npp + leaf_off + e % epp;
+          cb_rs[e + 1] = cb_rs[e] + (P.far_row_start[t + 1] - P.far_row_start[t]);
+        }
+        const double need = static_cast<double>(cb_rs[ne]) * NL * NL * 16.0;
+        if (frac > 0.0 && cb_rs[ne] > 0 && need <= 0.25 * static_cast<double>(available_device_bytes(device_))) {
+          std::vector<int> eb(cb_rs[ne]);
+#pragma omp parallel for schedule(static)
+          for (int e = 0; e < ne; ++e) {
+            const int t = (e / epp) * P.npp + leaf_off + e % epp;
+            for (int q = P.far_row_start[t], k = cb_rs[e]; q < P.far_row_start[t + 1]; ++q, ++k) {
+              const int sq = P.far_b[q];
+              eb[k] = (sq / P.npp) * epp + (sq % P.npp - leaf_off);
+            }
+          }
+          d_cb_rs_ = upload(cb_rs);
+          d_cb_eb_ = upload(eb);
+          d_cb_blk_ = dalloc<double>(static_cast<size_t>(cb_rs[ne]) * NL * NL * 2);
+          cblk_ = true;
+          n_leaf_blocks_ = cb_rs[ne] / 2;
+          leaf_block_bytes_ = static_cast<size_t>(cb_rs[ne]) * NL * NL * 16;
+          sym_pairs_[0] = 0;
+        }
+      }
+    };
     // symmetric fused far field (Laplace, m <= 6): upper pairs + transposes
     sym_far_ = !stored_couplings() && d.kind() == kLaplace && m >= 2 && m <= 6;
     // m <= 5, one GPU: the column-stream kernel, two columns per lane (c5:
@@ -659,36 +688,7 @@ void H2Device::stage_plan() {
           lb_lap("uploads");
         }
       }
-      // Helmholtz: all leaf-level far pairs as complex element blocks (ordered rows)
-      if (sym_w_ && d.is_complex() && ident && P.depth >= 1) {
-        double frac = 1.0;
-        if (const char* env = getenv("IGB_H2_LEAF_BLOCKS")) frac = atof(env);
-        const int ne = d.element_count(), epp = d.elements_per_patch(), leaf_off = P.level_offset[P.depth];
-        std::vector<int> cb_rs(ne + 1, 0);
-        for (int e = 0; e < ne; ++e) {
-          const int t = (e / epp) * P.npp + leaf_off + e % epp;
-          cb_rs[e + 1] = cb_rs[e] + (P.far_row_start[t + 1] - P.far_row_start[t]);
-        }
-        const double need = static_cast<double>(cb_rs[ne]) * NL * NL * 16.0;
-        if (frac > 0.0 && cb_rs[ne] > 0 && need <= 0.25 * static_cast<double>(available_device_bytes(device_))) {
-          std::vector<int> eb(cb_rs[ne]);
-#pragma omp parallel for schedule(static)
-          for (int e = 0; e < ne; ++e) {
-            const int t = (e / epp) * P.npp + leaf_off + e % epp;
-            for (int q = P.far_row_start[t], k = cb_rs[e]; q < P.far_row_start[t + 1]; ++q, ++k) {
-              const int sq = P.far_b[q];
-              eb[k] = (sq / P.npp) * epp + (sq % P.npp - leaf_off);
-            }
-          }
-          d_cb_rs_ = upload(cb_rs);
-          d_cb_eb_ = upload(eb);
-          d_cb_blk_ = dalloc<double>(static_cast<size_t>(cb_rs[ne]) * NL * NL * 2);
-          cblk_ = true;
-          n_leaf_blocks_ = cb_rs[ne] / 2;
-          leaf_block_bytes_ = static_cast<size_t>(cb_rs[ne]) * NL * NL * 16;
-          sym_pairs_[0] = 0;
-        }
-      }
+      if (sym_w_ && d.is_complex() && ident && P.depth >= 1) setup_cblk();
       if (Lp.world > 1 && sym_far_ && m <= 5) {  // per-target column lists for k_far_col_list
         std::vector<int> col_rs(1, 0), col_q;
         for (int t : sym_targets) {
@@ -708,6 +708,22 @@ void H2Device::stage_plan() {
       d_slot_ = dalloc<double>(P.far_a.size() * per_pair);
       // slots no kernel writes (multi-GPU: pairs with another rank's node) read as 0
       IGB_CUDA(cudaMemsetAsync(d_slot_, 0, P.far_a.size() * per_pair * sizeof(double), up_stream_ ? up_stream_ : stream_));
+    } else if (stored_couplings() && d.is_complex() && Lp.world == 1 && P.depth >= 2 && mm >= 32 && mm <= 128) {
+      // stored couplings streamed for the coarse levels only, the leaf level as element blocks
+      bool ident = static_cast<int>(Lp.el.size()) == d.element_count();
+      for (size_t i = 0; ident && i < Lp.el.size(); ++i) ident = Lp.el[i] == static_cast<int>(i);
+      if (ident) {
+        d_upper_start_ = upload(P.far_upper_start);
+        d_trans_ = upload(P.far_trans);
+        setup_cblk();
+        if (cblk_) {
+          std::vector<int> coarse;
+          for (int t : Lp.far_targets)
+            if (P.node_level[t] < P.depth) coarse.push_back(t);
+          n_far_coarse_ = static_cast<int>(coarse.size());
+          d_far_coarse_ = upload(coarse);
+        }
+      }
     }
   }
   d_dof_start_ = upload(Lp.dof_start);
@@ -1026,6 +1042,11 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
   if (n_far_targets_ > 0) {
     const unsigned grid = grid_for(static_cast<long long>(n_far_targets_) * 32, 256);
     if (stored_couplings()) {
+      // leaf blocks: the stored couplings of the coarse levels only
+      const bool cbs = cblk_ && !far_only_;
+      const int n_ft = cbs ? n_far_coarse_ : n_far_targets_;
+      const int* ft = cbs ? d_far_coarse_ : d_far_targets_;
+      const unsigned grid = grid_for(static_cast<long long>(std::max(n_ft, 1)) * 32, 256);
       S dw;
       if constexpr (sizeof(S) == 8) {
         dw = 1.0;
@@ -1035,26 +1056,27 @@ void H2Device::enqueue_phase2(const double* recv, double* yout, cudaStream_t s, 
         dw = mk(w.real(), w.imag());
       }
       const S* K = reinterpret_cast<const S*>(d_far_);
-      if (mm >= 32) {  // one CTA per target
+      if (n_ft == 0) {
+      } else if (mm >= 32) {  // one CTA per target
         const size_t smem = static_cast<size_t>(8) * nch_ * mm * sizeof(S);
-        const unsigned nt = static_cast<unsigned>(n_far_targets_);
+        const unsigned nt = static_cast<unsigned>(n_ft);
         if (nch_ == 4) {
-          if (mm <= 32) k_far_cta<S, 4, 1><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-          else if (mm <= 64) k_far_cta<S, 4, 2><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-          else k_far_cta<S, 4, 4><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          if (mm <= 32) k_far_cta<S, 4, 1><<<nt, 256, smem, s>>>(ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else if (mm <= 64) k_far_cta<S, 4, 2><<<nt, 256, smem, s>>>(ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else k_far_cta<S, 4, 4><<<nt, 256, smem, s>>>(ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
         } else {
-          if (mm <= 32) k_far_cta<S, 1, 1><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-          else if (mm <= 64) k_far_cta<S, 1, 2><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-          else k_far_cta<S, 1, 4><<<nt, 256, smem, s>>>(d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          if (mm <= 32) k_far_cta<S, 1, 1><<<nt, 256, smem, s>>>(ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else if (mm <= 64) k_far_cta<S, 1, 2><<<nt, 256, smem, s>>>(ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+          else k_far_cta<S, 1, 4><<<nt, 256, smem, s>>>(ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
         }
       } else if (nch_ == 4) {
-        if (mm <= 32) k_far<S, 4, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-        else if (mm <= 64) k_far<S, 4, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-        else k_far<S, 4, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        if (mm <= 32) k_far<S, 4, 1><<<grid, 256, 0, s>>>(n_ft, ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else if (mm <= 64) k_far<S, 4, 2><<<grid, 256, 0, s>>>(n_ft, ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else k_far<S, 4, 4><<<grid, 256, 0, s>>>(n_ft, ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
       } else {
-        if (mm <= 32) k_far<S, 1, 1><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-        else if (mm <= 64) k_far<S, 1, 2><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
-        else k_far<S, 1, 4><<<grid, 256, 0, s>>>(n_far_targets_, d_far_targets_, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        if (mm <= 32) k_far<S, 1, 1><<<grid, 256, 0, s>>>(n_ft, ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else if (mm <= 64) k_far<S, 1, 2><<<grid, 256, 0, s>>>(n_ft, ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
+        else k_far<S, 1, 4><<<grid, 256, 0, s>>>(n_ft, ft, d_far_rs_, d_far_b_, K, mm, up, dw, down);
       }
     } else if (sym_far_) {
       const unsigned gsym = grid_for(static_cast<long long>(n_sym_targets_) * 32, 256);
@@ -1576,7 +1598,7 @@ void H2Device::far_field(const double* x, double* up_out, double* down_out) {
   }
   far_only_ = false;
   IGB_CUDA(cudaStreamSynchronize(stream_));
-  if (n_leaf_blocks_ > 0)  // the blocked pairs' slots were written here; apply() never rewrites them
+  if (n_leaf_blocks_ > 0 && !cblk_)  // Laplace: the blocked pairs' slots were written here; apply() never rewrites them
     IGB_CUDA(cudaMemsetAsync(d_slot_, 0, plan_.far_a.size() * static_cast<size_t>(plan_.m) * plan_.m * sizeof(double), stream_));
   const size_t n = static_cast<size_t>(plan_.n_nodes) * nch_ * plan_.m * plan_.m * sw;
   if (up_out) IGB_CUDA(cudaMemcpy(up_out, d_up_, n, cudaMemcpyDeviceToHost));

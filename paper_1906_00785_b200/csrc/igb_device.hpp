@@ -180,6 +180,8 @@ class H2Device {
   // Helmholtz (one GPU): every leaf-level far pair as a complex element block in rows added
   // to the near rows (k_leaf_blocks_c / k_block_rows_acc); the far kernel keeps the coarse levels
   bool cblk_ = false;
+  int n_far_coarse_ = 0;
+  int* d_far_coarse_ = nullptr;  // stored couplings + blocks: the far targets above the leaf level
   int *d_cb_rs_ = nullptr, *d_cb_eb_ = nullptr;
   double* d_cb_blk_ = nullptr;
   int *d_low_rs_ = nullptr, *d_low_q_ = nullptr;  // per node: the lower pairs whose slots are written
